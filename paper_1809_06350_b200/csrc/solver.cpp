@@ -1,0 +1,508 @@
+// Device-resident Krylov solvers, AMG V-cycle and the nested block
+// preconditioner.  Control flow restates krylov.cpp:21-176 (GMRES/FGMRES),
+// amg.cpp:297-361 (V-cycle) and precond.cpp:26-109,157-218 (Schur operator,
+// SCR, nested preconditioner, solve_block_system).  Vectors never leave the
+// device; per Krylov iteration the host reads back the new Hessenberg column
+// (j+2 doubles) and runs the Givens rotations and the convergence test with
+// the reference's own scalar arithmetic.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+
+#include "ctx.hpp"
+
+namespace edb {
+
+double now_ms()
+{
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// ---------------------------------------------------------------------------
+// workspace
+
+void KrylovWs::ensure_n(int64_t nn)
+{
+    if (nn == n) return;
+    V.clear();
+    Z.clear();
+    hV.clear();
+    hZ.clear();
+    dV.release();
+    dZ.release();
+    n = nn;
+    r.alloc(n);
+    w.alloc(n);
+    t.alloc(n);
+}
+
+double* KrylovWs::v(int j)
+{
+    while (static_cast<int>(V.size()) <= j) {
+        V.emplace_back(static_cast<size_t>(n));
+        hV.push_back(V.back().p);
+    }
+    return V[j].p;
+}
+
+double* KrylovWs::z(int j)
+{
+    while (static_cast<int>(Z.size()) <= j) {
+        Z.emplace_back(static_cast<size_t>(n));
+        hZ.push_back(Z.back().p);
+    }
+    return Z[j].p;
+}
+
+void KrylovWs::sync_ptrs(cudaStream_t s)
+{
+    if (dV.n != hV.size()) dV.upload(hV.data(), hV.size(), s);
+    if (dZ.n != hZ.size()) dZ.upload(hZ.data(), hZ.size(), s);
+}
+
+size_t KrylovWs::bytes() const { return (V.size() + Z.size() + 3) * static_cast<size_t>(n) * sizeof(double); }
+
+namespace {
+
+double read_scalar(Ctx& c, const double* d)
+{
+    double* h = c.host_buf(1);
+    ED_CUDA(cudaMemcpyAsync(h, d, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    ED_CUDA(cudaStreamSynchronize(c.stream));
+    return h[0];
+}
+
+} // namespace
+
+// run_gmres, krylov.cpp:21-176
+SolveRes gmres_dev(Ctx& c, DOp& op, DPrec* M, const double* b, double* x, const KrylovCfg& cfg, bool flexible,
+                   KrylovWs& ws)
+{
+    if (cfg.restart < 1) throw Error(ED_INVALID_ARGUMENT, "gmres: restart must be >= 1");
+    cudaStream_t s = c.stream;
+    const int64_t n = op.size();
+    ws.ensure_n(n);
+    const int m = cfg.restart;
+    if (static_cast<int>(ws.hcol.n) < m + 2) ws.hcol.alloc(m + 2);
+    if (static_cast<int>(ws.corr.n) < m + 1) ws.corr.alloc(m + 1);
+    if (static_cast<int>(ws.ycoef.n) < m + 1) ws.ycoef.alloc(m + 1);
+    if (ws.scal.n < 8) ws.scal.alloc(8);
+    double* r = ws.r.p;
+    double* w = ws.w.p;
+    double* t = ws.t.p;
+    double* h = ws.hcol.p;
+    double* sc = ws.scal.p; // [0] |w|^2, [1] reorth flag, [2] wnorm, [3] norm scratch
+
+    SolveRes res;
+    op.apply(x, r);
+    vec_sub_from(r, b, n, s);
+    norm2(c.red, r, n, sc + 3, s);
+    double rnorm = read_scalar(c, sc + 3);
+    res.initial_norm = rnorm;
+    const double tol = std::max(cfg.rel_tol * rnorm, cfg.abs_tol);
+    if (rnorm <= tol) {
+        res.converged = true;
+        res.final_norm = rnorm;
+        return res;
+    }
+
+    std::vector<std::vector<double>> H(m);
+    std::vector<double> cs(m), sn(m), g(static_cast<size_t>(m) + 1), y;
+    int total = 0;
+    bool stagnated = false;
+    while (total < cfg.max_iters && !stagnated) {
+        norm2(c.red, r, n, sc + 3, s);
+        const double beta = read_scalar(c, sc + 3);
+        if (beta == 0.0) break;
+        vec_div_scalar(ws.v(0), r, sc + 3, nullptr, n, s);
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+
+        int j = 0;
+        bool breakdown = false;
+        while (j < m && total < cfg.max_iters) {
+            double* vj = ws.v(j);
+            if (M) {
+                if (flexible) {
+                    double* zj = ws.z(j);
+                    M->apply(vj, zj);
+                    op.apply(zj, w);
+                } else {
+                    M->apply(vj, t);
+                    op.apply(t, w);
+                }
+            } else {
+                op.apply(vj, w);
+            }
+            // modified Gram-Schmidt chain (krylov.cpp:81-86), one fused
+            // "w -= h_{i-1} v_{i-1}; h_i = v_i . w" pass per i
+            mgs_axpy_dot(c.red, w, nullptr, nullptr, ws.v(0), n, h + 0, s);
+            for (int i = 1; i <= j; ++i) mgs_axpy_dot(c.red, w, ws.v(i - 1), h + i - 1, ws.v(i), n, h + i, s);
+            mgs_axpy_dot(c.red, w, ws.v(j), h + j, nullptr, n, sc + 0, s);
+            double* vnext = ws.v(j + 1);
+            ws.sync_ptrs(s);
+            // always-computed classical check + selective reorthogonalization (:87-105)
+            multi_dot(c.red, ws.dV.p, j + 1, w, n, ws.corr.p, s);
+            reorth_decide(sc, h, ws.corr.p, j + 1, s);
+            reorth_apply(c.red, w, ws.dV.p, ws.corr.p, j + 1, n, sc, s);
+            vec_div_scalar(vnext, w, sc + 2, sc + 2, n, s);
+            double* hb = c.host_buf(static_cast<size_t>(j) + 8);
+            ED_CUDA(cudaMemcpyAsync(hb, h, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+            ED_CUDA(cudaMemcpyAsync(hb + j + 1, sc, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+            ED_CUDA(cudaStreamSynchronize(s));
+            std::vector<double>& hc = H[j];
+            hc.assign(hb, hb + j + 1);
+            const double wnorm = hb[j + 3];
+            hc.push_back(wnorm);
+            if (!(wnorm > 1e-300)) breakdown = true;
+            // Givens rotations (:114-131)
+            for (int i = 0; i < j; ++i) {
+                const double hi = hc[i], hi1 = hc[i + 1];
+                hc[i] = cs[i] * hi + sn[i] * hi1;
+                hc[i + 1] = -sn[i] * hi + cs[i] * hi1;
+            }
+            const double denom = std::hypot(hc[j], hc[j + 1]);
+            if (denom == 0.0) {
+                cs[j] = 1.0;
+                sn[j] = 0.0;
+            } else {
+                cs[j] = hc[j] / denom;
+                sn[j] = hc[j + 1] / denom;
+            }
+            hc[j] = denom;
+            hc[j + 1] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] *= cs[j];
+            ++total;
+            ++j;
+            const double est = std::abs(g[j]);
+            res.history.push_back(est);
+            if (est <= tol || breakdown) break;
+        }
+        // back substitution (:140-146)
+        y.assign(j, 0.0);
+        for (int i = j - 1; i >= 0; --i) {
+            double sum = g[i];
+            for (int k = i + 1; k < j; ++k) sum -= H[k][i] * y[k];
+            y[i] = (H[i][i] != 0.0) ? sum / H[i][i] : 0.0;
+        }
+        if (j > 0) ED_CUDA(cudaMemcpyAsync(ws.ycoef.p, y.data(), j * sizeof(double), cudaMemcpyHostToDevice, s));
+        ws.sync_ptrs(s);
+        if (flexible && M) {
+            multi_axpy(x, ws.dZ.p, ws.ycoef.p, j, n, s);
+        } else {
+            vec_fill(t, 0.0, n, s);
+            multi_axpy(t, ws.dV.p, ws.ycoef.p, j, n, s);
+            if (M) {
+                M->apply(t, w);
+                vec_add(x, w, n, s);
+            } else {
+                vec_add(x, t, n, s);
+            }
+        }
+        // true residual at the restart boundary (:161-170)
+        op.apply(x, r);
+        vec_sub_from(r, b, n, s);
+        norm2(c.red, r, n, sc + 3, s);
+        rnorm = read_scalar(c, sc + 3);
+        if (rnorm <= tol) {
+            res.converged = true;
+            break;
+        }
+        if (breakdown) stagnated = true;
+    }
+    res.iterations = total;
+    res.final_norm = rnorm;
+    return res;
+}
+
+// ---------------------------------------------------------------------------
+// AMG
+
+void DevHierarchy::build(Ctx& c, const Sell& A0, const AmgOpts& o)
+{
+    cudaStream_t s = c.stream;
+    opts = o;
+    lv.clear();
+    fallback = false;
+    const double t0 = now_ms();
+    const HostCsr A0h = sell_to_csr(A0, s);
+    const HostHierarchy hh = amg_build_host(A0h, o);
+    setup_host_ms = now_ms() - t0;
+    if (hh.fallback) {
+        fallback = true;
+        fb_invd.upload(hh.fallback_inv_diag, s);
+        ED_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    const int L = static_cast<int>(hh.levels.size());
+    const int Bc = (o.block_size == 3) ? 3 : 1;
+    lv.resize(L);
+    for (int l = 0; l < L; ++l) {
+        DevLevel& d = lv[l];
+        const HostLevel& H = hh.levels[l];
+        d.n = H.A.nrows;
+        const int Bl = (l == 0) ? A0.st->Rb : Bc;
+        if (l == 0) {
+            d.A = &A0;
+        } else {
+            d.Aown = sell_from_csr(H.A, Bl, Bl, true, s);
+            d.A = &d.Aown;
+        }
+        d.invd.upload(H.inv_diag, s);
+        d.s.alloc(d.n);
+        if (l > 0) {
+            d.r.alloc(d.n);
+            d.z.alloc(d.n);
+        }
+        if (l + 1 < L) {
+            d.P = sell_from_csr(H.P, Bl, Bc, false, s);
+            d.R = sell_from_csr(H.R, Bc, Bl, false, s);
+        }
+    }
+    nc = hh.nc;
+    pinv.upload(hh.pinv, s);
+    ED_CUDA(cudaStreamSynchronize(s));
+}
+
+// AmgHierarchy::smooth, amg.cpp:297-324
+void DevHierarchy::smooth(Ctx& c, int l, const double* b, double* z, int sweeps)
+{
+    DevLevel& d = lv[l];
+    if (opts.smoother == 0) {
+        for (int k = 0; k < sweeps; ++k) {
+            spmv(*d.A, z, d.s.p, nullptr, 0, c.stream);
+            jacobi_update(z, b, d.s.p, d.invd.p, opts.jacobi_weight, d.n, c.stream);
+        }
+        return;
+    }
+    for (int k = 0; k < sweeps; ++k) {
+        sgs_sweep(*d.A, b, z, d.invd.p, true, c.stream);
+        sgs_sweep(*d.A, b, z, d.invd.p, false, c.stream);
+    }
+}
+
+// AmgHierarchy::cycle, amg.cpp:326-352
+void DevHierarchy::cycle(Ctx& c, int l, const double* r, double* z)
+{
+    DevLevel& d = lv[l];
+    cudaStream_t s = c.stream;
+    if (l == n_levels() - 1) {
+        dense_gemv(pinv.p, r, z, nc, s); // COD min-norm solve (amg.cpp:331-334)
+        return;
+    }
+    vec_fill(z, 0.0, d.n, s);
+    smooth(c, l, r, z, opts.pre_sweeps);
+    spmv(*d.A, z, d.s.p, r, 1, s); // scratch = r - A z
+    DevLevel& e = lv[l + 1];
+    spmv(d.R, d.s.p, e.r.p, nullptr, 0, s);
+    cycle(c, l + 1, e.r.p, e.z.p);
+    spmv(d.P, e.z.p, z, nullptr, 2, s); // z += P zc
+    smooth(c, l, r, z, opts.post_sweeps);
+}
+
+void DevHierarchy::vcycle(Ctx& c, const double* r, double* z)
+{
+    if (fallback) {
+        vec_copy(z, r, static_cast<int64_t>(fb_invd.n), c.stream);
+        vec_mul(z, fb_invd.p, static_cast<int64_t>(fb_invd.n), c.stream);
+        return;
+    }
+    cycle(c, 0, r, z);
+}
+
+// ---------------------------------------------------------------------------
+// operators
+
+namespace {
+
+struct SellOp final : DOp {
+    const Sell& M;
+    cudaStream_t s;
+    SellOp(const Sell& m, cudaStream_t st) : M(m), s(st) {}
+    int64_t size() const override { return M.nrows(); }
+    void apply(const double* x, double* y) override { spmv(M, x, y, nullptr, 0, s); }
+};
+
+// BlockOperator (blocksystem.hpp:27-45)
+struct BlockOp final : DOp {
+    WorkSys& W;
+    cudaStream_t s;
+    BlockOp(WorkSys& w, cudaStream_t st) : W(w), s(st) {}
+    int64_t size() const override { return static_cast<int64_t>(W.nv) + W.np; }
+    void apply(const double* x, double* y) override
+    {
+        spmv2(W.A, x, W.B, x + W.nv, y, 1.0, s);
+        spmv2(W.C, x, W.D, x + W.nv, y + W.nv, 1.0, s);
+    }
+};
+
+struct AmgPrec final : DPrec {
+    Ctx& c;
+    DevHierarchy& h;
+    AmgPrec(Ctx& cc, DevHierarchy& hh) : c(cc), h(hh) {}
+    void apply(const double* r, double* z) override { h.vcycle(c, r, z); }
+};
+
+KrylovCfg kcfg(const ed_krylov_config& k) { return KrylovCfg{k.restart, k.max_iters, k.rel_tol, k.abs_tol}; }
+
+// SchurOperator::apply, precond.cpp:26-42
+struct SchurOp final : DOp {
+    Ctx& c;
+    WorkSys& W;
+    DevHierarchy& amg_a;
+    KrylovCfg cfg;
+    Stats& st;
+    DevArray<double> t, z;
+    SchurOp(Ctx& cc, WorkSys& w, DevHierarchy& a, const KrylovCfg& k, Stats& sts)
+        : c(cc), W(w), amg_a(a), cfg(k), st(sts), t(w.nv), z(w.nv)
+    {
+    }
+    int64_t size() const override { return W.np; }
+    void apply(const double* x, double* y) override
+    {
+        spmv(W.B, x, t.p, nullptr, 0, c.stream);
+        vec_fill(z.p, 0.0, W.nv, c.stream);
+        SellOp aop(W.A, c.stream);
+        AmgPrec M(c, amg_a);
+        const SolveRes r = gmres_dev(c, aop, &M, t.p, z.p, cfg, false, c.ws_a);
+        st.schur_applies += 1;
+        st.inner_iters += r.iterations;
+        spmv2(W.D, x, W.C, z.p, y, -1.0, c.stream); // y = D x - C z
+    }
+};
+
+// ScrSolver::solve, precond.cpp:52-99
+struct Scr {
+    Ctx& c;
+    WorkSys& W;
+    KrylovCfg ta, ts, ti;
+    DevHierarchy& amg_a;
+    DevHierarchy& amg_s;
+    Stats& st;
+    DevArray<double> xhat, rp2, rv2;
+    Scr(Ctx& cc, WorkSys& w, const ed_block_solver_options& o, DevHierarchy& a, DevHierarchy& sh, Stats& sts)
+        : c(cc), W(w), ta(kcfg(o.a)), ts(kcfg(o.s)), ti(kcfg(o.inner)), amg_a(a), amg_s(sh), st(sts),
+          xhat(w.nv), rp2(w.np), rv2(w.nv)
+    {
+    }
+    void solve(const double* rv, const double* rp, double* xv, double* xp)
+    {
+        cudaStream_t s = c.stream;
+        SellOp aop(W.A, s);
+        AmgPrec Ma(c, amg_a), Ms(c, amg_s);
+        // 1. A xhat = r_v
+        vec_fill(xhat.p, 0.0, W.nv, s);
+        SolveRes r1 = gmres_dev(c, aop, &Ma, rv, xhat.p, ta, false, c.ws_a);
+        st.a_solves += 1;
+        st.a_iters += r1.iterations;
+        // 2. r_p - C xhat
+        spmv(W.C, xhat.p, rp2.p, rp, 1, s);
+        // 3. S x_p = r_p
+        vec_fill(xp, 0.0, W.np, s);
+        if (ti.rel_tol >= 1.0) {
+            SellOp sop(W.S, s);
+            SolveRes r3 = gmres_dev(c, sop, &Ms, rp2.p, xp, ts, false, c.ws_s);
+            st.s_solves += 1;
+            st.s_iters += r3.iterations;
+        } else {
+            SchurOp sop(c, W, amg_a, ti, st);
+            SolveRes r3 = gmres_dev(c, sop, &Ms, rp2.p, xp, ts, false, c.ws_s);
+            st.s_solves += 1;
+            st.s_iters += r3.iterations;
+        }
+        // 4. r_v - B x_p
+        spmv(W.B, xp, rv2.p, rv, 1, s);
+        // 5. A x_v = r_v
+        vec_fill(xv, 0.0, W.nv, s);
+        SolveRes r5 = gmres_dev(c, aop, &Ma, rv2.p, xv, ta, false, c.ws_a);
+        st.a_solves += 1;
+        st.a_iters += r5.iterations;
+    }
+};
+
+// NestedPrecond::apply, precond.cpp:101-109
+struct NestedPrec final : DPrec {
+    Scr& scr;
+    int nv;
+    explicit NestedPrec(Scr& s, int nvv) : scr(s), nv(nvv) {}
+    void apply(const double* r, double* z) override { scr.solve(r, r + nv, z, z + nv); }
+};
+
+} // namespace
+
+AmgOpts amg_opts_from(const ed_amg_options& o, const Ctx& c, bool velocity, int nrows)
+{
+    AmgOpts a;
+    a.block_size = o.block_size;
+    a.strength_theta = o.strength_theta;
+    a.max_levels = o.max_levels;
+    a.coarse_max_rows = o.coarse_max_rows;
+    a.smoother = o.smoother;
+    a.jacobi_weight = o.jacobi_weight;
+    a.pre_sweeps = o.pre_sweeps;
+    a.post_sweeps = o.post_sweeps;
+    a.smooth_prolongator = o.smooth_prolongator != 0;
+    if (velocity && o.use_dof_row_maps && c.have_dofs && c.sys_from_mesh && nrows == 3 * c.nfree) {
+        // set_amg_maps (driver.cpp:32-48): compressed free-node ids, component
+        a.row_to_node.resize(nrows);
+        a.row_component.resize(nrows);
+        for (int r = 0; r < nrows; ++r) {
+            a.row_to_node[r] = r / 3;
+            a.row_component[r] = r % 3;
+        }
+    }
+    return a;
+}
+
+// solve_block_system, precond.cpp:157-218 (Nested branch)
+Stats solve_block_system_dev(Ctx& c, const double* d_rhs, double* d_x, const ed_block_solver_options& o,
+                             std::vector<double>* history, ed_phase_times* times)
+{
+    if (o.precond != 0) throw Error(ED_UNSUPPORTED, "only the nested preconditioner is built (PrecondKind::Nested)");
+    const double t0 = now_ms();
+    cudaStream_t s = c.stream;
+    Stats st;
+    WorkSys& W = c.work; // solver working set (reused across solves)
+    double tp = now_ms();
+    make_work(c, W, o.scale != 0, o.eps_diag);
+    const int64_t n = static_cast<int64_t>(W.nv) + W.np;
+    DevArray<double> b(n);
+    vec_copy(b.p, d_rhs, n, s);
+    if (W.scaled) vec_mul(b.p, W.w.p, n, s);
+    vec_fill(d_x, 0.0, n, s);
+    c.sync();
+    const double t_planes = now_ms() - tp;
+    tp = now_ms();
+    build_shat_work(c, W);
+    c.sync();
+    const double t_shat = now_ms() - tp;
+    tp = now_ms();
+    DevHierarchy amg_a, amg_s;
+    amg_a.build(c, W.A, amg_opts_from(o.amg_a, c, true, W.nv));
+    amg_s.build(c, W.S, amg_opts_from(o.amg_s, c, false, W.np));
+    c.sync();
+    const double t_amg = now_ms() - tp;
+    tp = now_ms();
+    Scr scr(c, W, o, amg_a, amg_s, st);
+    NestedPrec M(scr, W.nv);
+    BlockOp op(W, s);
+    const SolveRes res = gmres_dev(c, op, &M, b.p, d_x, kcfg(o.outer), true, c.ws_outer);
+    if (W.scaled) vec_mul(d_x, W.w.p, n, s);
+    c.sync();
+    const double t_fg = now_ms() - tp;
+    st.outer_iters = res.iterations;
+    st.converged = res.converged;
+    st.t_solve = (now_ms() - t0) * 1e-3;
+    if (history) *history = res.history;
+    if (times) {
+        times->planes_ms = t_planes;
+        times->shat_ms = t_shat;
+        times->amg_setup_ms = t_amg;
+        times->amg_host_ms = amg_a.setup_host_ms + amg_s.setup_host_ms;
+        times->fgmres_ms = t_fg;
+    }
+    return st;
+}
+
+} // namespace edb
