@@ -8,6 +8,9 @@
 #include <cmath>
 #include <limits>
 #include <numeric>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 namespace edb {
 
@@ -542,8 +545,24 @@ std::vector<double> cod_pinv(const std::vector<double>& dense_colmajor, int n, d
 }
 
 // AmgHierarchy::build, amg.cpp:189-295
+namespace {
+struct StageTimer {
+    bool on = std::getenv("ED_AMG_VERBOSE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void lap(const char* what, int level, long rows, long nnz)
+    {
+        const auto now = std::chrono::steady_clock::now();
+        if (on)
+            std::fprintf(stderr, "[amg] L%d %-12s %9.3f s  rows %ld nnz %ld\n", level, what,
+                         std::chrono::duration<double>(now - t).count(), rows, nnz);
+        t = now;
+    }
+};
+} // namespace
+
 HostHierarchy amg_build_host(const HostCsr& A0, const AmgOpts& opts)
 {
+    StageTimer T;
     if (A0.nrows != A0.ncols) throw Error(ED_INVALID_ARGUMENT, "amg: matrix must be square");
     const int k = opts.block_size;
     if (k < 1) throw Error(ED_INVALID_ARGUMENT, "amg: block size must be positive");
@@ -570,9 +589,13 @@ HostHierarchy amg_build_host(const HostCsr& A0, const AmgOpts& opts)
     HostCsr A = A0;
     while (A.nrows > opts.coarse_max_rows && static_cast<int>(h.levels.size()) + 1 < opts.max_levels) {
         const int n_nodes = node_of_row.empty() ? 0 : node_of_row.back() + 1;
+        const int lvl = static_cast<int>(h.levels.size());
+        T.lap("start", lvl, A.nrows, A.nnz());
         const auto nbr = strong_neighbors(A, node_of_row, n_nodes, opts.strength_theta);
+        T.lap("strength", lvl, A.nrows, A.nnz());
         std::vector<int> agg_of_node;
         const int n_agg = aggregate(nbr, agg_of_node);
+        T.lap("aggregate", lvl, n_agg, 0);
         if (n_agg <= 0 || n_agg >= n_nodes) {
             if (h.levels.empty()) {
                 h.fallback = true;
@@ -585,19 +608,27 @@ HostHierarchy amg_build_host(const HostCsr& A0, const AmgOpts& opts)
         for (int r = 0; r < A.nrows; ++r) agg_of_row[r] = agg_of_node[node_of_row[r]];
         std::vector<double> Bc;
         HostCsr P = tentative_prolongator(A.nrows, k, agg_of_row, n_agg, B, Bc);
+        T.lap("tentative", lvl, P.nrows, P.nnz());
         HostLevel lv;
         lv.inv_diag = inverted_diag(A);
         if (opts.smooth_prolongator) {
             const double lambda = estimate_spectral_radius(A, lv.inv_diag);
+            T.lap("spectral", lvl, A.nrows, 0);
             const double omega = 4.0 / (3.0 * std::max(lambda, 1e-12));
             HostCsr AP = csr_matmul(A, P);
+            T.lap("AP_tent", lvl, AP.nrows, AP.nnz());
 #pragma omp parallel for schedule(static)
             for (int r = 0; r < AP.nrows; ++r)
                 for (int kk = AP.rowptr[r]; kk < AP.rowptr[r + 1]; ++kk) AP.val[kk] *= lv.inv_diag[r];
             P = csr_add(P, AP, 1.0, -omega);
+            T.lap("smooth_P", lvl, P.nrows, P.nnz());
         }
         HostCsr R = csr_transpose(P);
-        HostCsr Ac = csr_matmul(R, csr_matmul(A, P));
+        T.lap("transpose", lvl, R.nrows, R.nnz());
+        HostCsr AP2 = csr_matmul(A, P);
+        T.lap("AP", lvl, AP2.nrows, AP2.nnz());
+        HostCsr Ac = csr_matmul(R, AP2);
+        T.lap("RAP", lvl, Ac.nrows, Ac.nnz());
         lv.A = std::move(A);
         lv.P = std::move(P);
         lv.R = std::move(R);
@@ -624,6 +655,7 @@ HostHierarchy amg_build_host(const HostCsr& A0, const AmgOpts& opts)
         for (int kk = Ac.rowptr[r]; kk < Ac.rowptr[r + 1]; ++kk)
             dense[static_cast<size_t>(Ac.col[kk]) * Ac.nrows + r] = Ac.val[kk];
     h.pinv = cod_pinv(dense, Ac.nrows, 1e-12);
+    T.lap("coarse_cod", static_cast<int>(h.levels.size()) - 1, Ac.nrows, Ac.nnz());
     return h;
 }
 

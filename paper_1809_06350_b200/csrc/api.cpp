@@ -4,7 +4,11 @@
 #include <atomic>
 #include <climits>
 #include <cmath>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 
 #include <omp.h>
 
@@ -14,6 +18,23 @@ namespace edb {
 
 namespace {
 std::atomic<int64_t> g_launches{0};
+// ED_PROFILE=1: synchronise after every launch and attribute wall time per
+// kernel name (diagnostic only; never set for measurements).
+struct KProf {
+    bool on = std::getenv("ED_PROFILE") != nullptr;
+    std::map<std::string, std::pair<int64_t, double>> t;
+    std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+    ~KProf()
+    {
+        if (!on) return;
+        std::vector<std::pair<double, std::string>> v;
+        for (auto& kv : t) v.push_back({kv.second.second, kv.first});
+        std::sort(v.rbegin(), v.rend());
+        for (auto& x : v)
+            std::fprintf(stderr, "[prof] %-22s %10.3f ms  %9lld launches\n", x.second.c_str(), x.first * 1e3,
+                         static_cast<long long>(t[x.second].first));
+    }
+} g_prof;
 }
 
 void after_launch(const char* what)
@@ -21,6 +42,14 @@ void after_launch(const char* what)
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const cudaError_t e = cudaPeekAtLastError();
     if (e != cudaSuccess) throw Error(ED_CUDA_ERROR, std::string("launch ") + what + ": " + cudaGetErrorString(e));
+    if (g_prof.on) {
+        cudaDeviceSynchronize();
+        const auto now = std::chrono::steady_clock::now();
+        auto& slot = g_prof.t[what];
+        slot.first += 1;
+        slot.second += std::chrono::duration<double>(now - g_prof.last).count();
+        g_prof.last = now;
+    }
 }
 
 int64_t launch_count() { return g_launches.load(); }
@@ -422,8 +451,8 @@ int ed_tangent_export(ed_ctx* ctx, int which, int32_t* dims, int32_t* rowptr, in
     return guarded(ctx, [&](Ctx& c) {
         ensure_system(c, nullptr);
         check(which >= 0 && which < 4, ED_INVALID_ARGUMENT, "plane must be 0..3");
-        const Sell* m[4] = {&c.sys.A, &c.sys.B, &c.sys.C, &c.sys.D};
-        const HostCsr a = sell_to_csr(*m[which], c.stream);
+        const Bsr* m[4] = {&c.sys.A, &c.sys.B, &c.sys.C, &c.sys.D};
+        const HostCsr a = bsr_to_csr(*m[which], c.stream);
         if (dims) {
             dims[0] = a.nrows;
             dims[1] = a.ncols;
@@ -651,12 +680,12 @@ int ed_gmres_a(ed_ctx* ctx, const double* b, double* x, const ed_krylov_config* 
         if (amg) o.amg_a = *amg;
         else o.amg_a.block_size = 1;
         ensure_system(c, &o);
-        const Sell& A = c.sys.A;
+        const Bsr& A = c.sys.A;
         const int n = A.nrows();
         struct Op final : DOp {
-            const Sell& M;
+            const Bsr& M;
             cudaStream_t s;
-            Op(const Sell& m, cudaStream_t st) : M(m), s(st) {}
+            Op(const Bsr& m, cudaStream_t st) : M(m), s(st) {}
             int64_t size() const override { return M.nrows(); }
             void apply(const double* xx, double* yy) override { spmv(M, xx, yy, nullptr, 0, s); }
         } op(A, c.stream);
@@ -679,7 +708,7 @@ int ed_gmres_a(ed_ctx* ctx, const double* b, double* x, const ed_krylov_config* 
         DPrec* M = nullptr;
         if (precond == 1) {
             DevArray<double> d(n);
-            sell_diag(A, d.p, c.stream);
+            bsr_diag(A, d.p, c.stream);
             jac.invd.alloc(n);
             inv_diag_from(d.p, jac.invd.p, n, c.stream);
             jac.s = c.stream;
@@ -716,7 +745,7 @@ int ed_amg_vcycle(ed_ctx* ctx, int which, const ed_block_solver_options* opts, c
         check(opts && r && z, ED_INVALID_ARGUMENT, "null argument");
         ensure_system(c, opts);
         DevHierarchy h;
-        const Sell* A = nullptr;
+        const Bsr* A = nullptr;
         if (which == 0) {
             A = &c.sys.A;
             h.build(c, *A, amg_opts_from(opts->amg_a, c, true, A->nrows()));
@@ -749,7 +778,7 @@ int ed_shat_export(ed_ctx* ctx, const ed_block_solver_options* opts, int32_t* di
         ensure_system(c, opts);
         make_work(c, c.work, opts->scale != 0, opts->eps_diag);
         build_shat_work(c, c.work);
-        const HostCsr a = sell_to_csr(c.work.S, c.stream);
+        const HostCsr a = bsr_to_csr(c.work.S, c.stream);
         if (dims) {
             dims[0] = a.nrows;
             dims[1] = a.ncols;

@@ -30,8 +30,7 @@ void launch_residual(const AsmArgs& A, const std::vector<int>& color_ptr, cudaSt
 void launch_tangent(const AsmArgs& A, const std::vector<int>& color_ptr, cudaStream_t s);
 void launch_traction(const int64_t* rowptr, const int* rows, const double* vals, int nrows_with, double* r_m,
                      cudaStream_t s);
-void launch_k4_to_plane(int plane, const int* src, const double* k4, double* val, int64_t nslot_lanes,
-                        cudaStream_t s);
+void launch_k4_to_plane(int plane, const int* src, const double* k4, double* val, int64_t nnzb, cudaStream_t s);
 
 // ---- system kernels (kernels_system.cu) ----
 // max |x_i| over [0, n) into *out (deterministic)
@@ -44,32 +43,27 @@ void block_weights(const double* da, const double* dd, int nv, int np, const dou
 void shat_inv_diag(const double* da, double* inv_da, int nv, double eps, int* bad_row, cudaStream_t s);
 
 struct ShatArgs {
-    // S_hat SELL (rows = pressure nodes, 1x1)
-    const int64_t* s_soff;
+    // S_hat (rows = pressure nodes, 1x1 blocks, stored in level order)
+    const int* s_rowptr;
     const int* s_perm;
-    const int* s_rowlen;
     double* s_val;
-    int s_nslices;
-    // C plane (rows = pressure nodes, 1 x Bv) and D (1x1) share a row layout
-    const int64_t* c_soff;
-    const int* c_rowlen;
+    int s_nrows;
+    // C plane (pressure rows, 1 x Bv) and D (1x1), natural row order
+    const int* c_rowptr;
     const int* c_col;
-    const int* c_inv;
     const double* c_val;
-    const int64_t* d_soff;
-    const int* d_rowlen;
+    const int* d_rowptr;
     const double* d_val;
-    // B plane (rows = velocity nodes, Bv x 1)
-    const int64_t* b_soff;
-    const int* b_rowlen;
+    // B plane (velocity block rows, Bv x 1), stored in A's level order
+    const int* b_rowptr;
     const int* b_inv;
     const double* b_val;
     const double* inv_da;
     // position maps
-    const int64_t* cb_off;   // per pressure row
-    const uint16_t* cb_pos;  // per (C block, B block) pair
+    const int64_t* cb_off;  // per pressure row
+    const uint16_t* cb_pos; // per (C block, B block) pair
     const int64_t* d_off;
-    const uint16_t* d_pos;   // per D block
+    const uint16_t* d_pos;  // per D block
     int Bv;
 };
 void launch_shat_numeric(const ShatArgs& a, cudaStream_t s);

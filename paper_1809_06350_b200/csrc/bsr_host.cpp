@@ -1,0 +1,268 @@
+// Host construction of level-ordered BSR operators, Gauss-Seidel level
+// schedules and dataflow work items.  Structure is
+// mesh-static: built once per mesh (or per AMG level); only values move per
+// Newton step.
+#include <algorithm>
+#include <numeric>
+
+#include "ed_internal.hpp"
+
+namespace edb {
+
+double Bsr::bytes_per_spmv() const
+{
+    const BsrStruct& S = *st;
+    const double blk = 8.0 * S.Rb * S.Cb + 4.0;
+    return static_cast<double>(S.nnzb) * blk + 4.0 * (S.nbr + 1) + 8.0 * S.nbr * S.Rb + 8.0 * S.nbc * S.Cb;
+}
+
+void gs_level_order(const BlockPattern& pat, std::vector<int>& order, std::vector<int>& level_of_pos, int& nlev)
+{
+    const int n = pat.nbr;
+    std::vector<int> level(n, 0);
+    nlev = n > 0 ? 1 : 0;
+    // Row i reads the NEW value of every j < i it couples to (amg.cpp:311-316),
+    // so it sits one level above the highest such j.
+    for (int i = 0; i < n; ++i) {
+        int lv = 0;
+        for (int64_t k = pat.rowptr[i]; k < pat.rowptr[i + 1]; ++k) {
+            const int j = pat.col[k];
+            if (j < i) lv = std::max(lv, level[j] + 1);
+        }
+        level[i] = lv;
+        nlev = std::max(nlev, lv + 1);
+    }
+    std::vector<int> cnt(nlev + 1, 0);
+    for (int i = 0; i < n; ++i) ++cnt[level[i] + 1];
+    for (int l = 0; l < nlev; ++l) cnt[l + 1] += cnt[l];
+    order.assign(n, 0);
+    level_of_pos.assign(n, 0);
+    for (int i = 0; i < n; ++i) {
+        const int pos = cnt[level[i]]++;
+        order[pos] = i;
+        level_of_pos[pos] = level[i];
+    }
+}
+
+bool pattern_symmetric(const BlockPattern& pat)
+{
+    if (pat.nbr != pat.nbc) return false;
+    for (int i = 0; i < pat.nbr; ++i)
+        for (int64_t k = pat.rowptr[i]; k < pat.rowptr[i + 1]; ++k) {
+            const int j = pat.col[k];
+            const auto b = pat.col.begin() + pat.rowptr[j];
+            const auto e = pat.col.begin() + pat.rowptr[j + 1];
+            if (!std::binary_search(b, e, i)) return false;
+        }
+    return true;
+}
+
+BsrLayout make_layout(const BlockPattern& pat, const std::vector<int>& row_order, const std::vector<int>& level_of_pos)
+{
+    BsrLayout L;
+    const int n = pat.nbr;
+    L.perm = row_order;
+    L.inv.assign(n, -1);
+    for (int s = 0; s < n; ++s) L.inv[row_order[s]] = s;
+    L.lev_ptr.push_back(0);
+    for (int s = 1; s < n; ++s)
+        if (!level_of_pos.empty() && level_of_pos[s] != level_of_pos[s - 1]) L.lev_ptr.push_back(s);
+    L.lev_ptr.push_back(n);
+    std::vector<int64_t> srp(n + 1, 0);
+    for (int s = 0; s < n; ++s) {
+        const int r = row_order[s];
+        srp[s + 1] = srp[s] + (pat.rowptr[r + 1] - pat.rowptr[r]);
+    }
+    L.addr.assign(pat.nnzb(), -1);
+    for (int r = 0; r < n; ++r)
+        for (int64_t k = pat.rowptr[r]; k < pat.rowptr[r + 1]; ++k) L.addr[k] = srp[L.inv[r]] + (k - pat.rowptr[r]);
+    return L;
+}
+
+static int auto_lanes(double avg_blocks)
+{
+    int L = 2;
+    while (L < 32 && L * 2 < avg_blocks) L *= 2;
+    return L;
+}
+
+std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLayout& lay, int Rb, int Cb,
+                                           cudaStream_t s, int lanes)
+{
+    if (pat.nnzb() >= (1LL << 31)) throw Error(ED_UNSUPPORTED, "operator exceeds int32 block indices");
+    auto st = std::make_shared<BsrStruct>();
+    BsrStruct& S = *st;
+    S.Rb = Rb;
+    S.Cb = Cb;
+    S.nbr = pat.nbr;
+    S.nbc = pat.nbc;
+    S.nnzb = pat.nnzb();
+    const int n = pat.nbr;
+    S.L = lanes > 0 ? lanes : auto_lanes(n > 0 ? static_cast<double>(S.nnzb) / n : 1.0);
+    S.h_rowptr.assign(n + 1, 0);
+    S.h_col.assign(S.nnzb, 0);
+    bool identity = true;
+    for (int s2 = 0; s2 < n; ++s2) identity = identity && lay.perm[s2] == s2;
+    std::vector<int> dpos(n, -1);
+    for (int s2 = 0; s2 < n; ++s2) {
+        const int r = lay.perm[s2];
+        const int64_t len = pat.rowptr[r + 1] - pat.rowptr[r];
+        S.h_rowptr[s2 + 1] = static_cast<int>(S.h_rowptr[s2] + len);
+        for (int64_t k = 0; k < len; ++k) {
+            const int c = pat.col[pat.rowptr[r] + k];
+            S.h_col[S.h_rowptr[s2] + k] = c;
+            if (c == r && pat.nbr == pat.nbc) dpos[s2] = static_cast<int>(S.h_rowptr[s2] + k);
+        }
+    }
+    if (!identity) {
+        S.h_perm = lay.perm;
+        S.h_inv = lay.inv;
+        S.perm.upload(S.h_perm, s);
+        S.inv.upload(S.h_inv, s);
+    }
+    S.lev_ptr = lay.lev_ptr;
+    S.leveled = !identity || S.lev_ptr.size() > 2;
+    S.rowptr.upload(S.h_rowptr, s);
+    S.col.upload(S.h_col, s);
+    if (pat.nbr == pat.nbc) S.dpos.upload(dpos, s);
+    // dataflow items: rows_per_item rows of one level each (256 threads / L lanes)
+    const int nlev = S.nlev();
+    S.rows_per_item = 256 / S.L;
+    std::vector<int> irow{0}, ilev, lcnt(std::max(nlev, 1), 0);
+    for (int l = 0; l < nlev; ++l)
+        for (int r0 = S.lev_ptr[l]; r0 < S.lev_ptr[l + 1]; r0 += S.rows_per_item) {
+            irow.push_back(std::min(r0 + S.rows_per_item, S.lev_ptr[l + 1]));
+            ilev.push_back(l);
+            ++lcnt[l];
+        }
+    S.nitems = static_cast<int>(ilev.size());
+    S.item_row.upload(irow, s);
+    S.item_level.upload(ilev, s);
+    S.lev_items.upload(lcnt, s);
+    S.sync.alloc(static_cast<size_t>(std::max(nlev, 1)) + 2);
+    S.sync.zero(s);
+    ED_CUDA(cudaStreamSynchronize(s)); // host vectors die at return
+    return st;
+}
+
+std::vector<double> bsr_pack_values(const BsrStruct& st, const BsrLayout& lay, const std::vector<double>& bvals)
+{
+    const int E = st.Rb * st.Cb;
+    std::vector<double> v(static_cast<size_t>(st.nval()), 0.0);
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < static_cast<int64_t>(lay.addr.size()); ++k)
+        for (int e = 0; e < E; ++e) v[lay.addr[k] * E + e] = bvals[k * E + e];
+    return v;
+}
+
+BlockPattern block_pattern_of_csr(const HostCsr& a, int Rb, int Cb)
+{
+    if (a.nrows % Rb != 0 || a.ncols % Cb != 0)
+        throw Error(ED_INVALID_ARGUMENT, "matrix size is not a multiple of the block size");
+    BlockPattern p;
+    p.nbr = a.nrows / Rb;
+    p.nbc = a.ncols / Cb;
+    p.rowptr.assign(p.nbr + 1, 0);
+    std::vector<std::vector<int>> rows(p.nbr);
+#pragma omp parallel
+    {
+        std::vector<int> mark(p.nbc, -1);
+#pragma omp for schedule(dynamic, 1024)
+        for (int I = 0; I < p.nbr; ++I) {
+            auto& cols = rows[I];
+            for (int r = I * Rb; r < (I + 1) * Rb; ++r)
+                for (int k = a.rowptr[r]; k < a.rowptr[r + 1]; ++k) {
+                    const int J = a.col[k] / Cb;
+                    if (mark[J] != I) {
+                        mark[J] = I;
+                        cols.push_back(J);
+                    }
+                }
+            std::sort(cols.begin(), cols.end());
+        }
+    }
+    for (int I = 0; I < p.nbr; ++I) p.rowptr[I + 1] = p.rowptr[I] + static_cast<int64_t>(rows[I].size());
+    p.col.resize(p.rowptr[p.nbr]);
+#pragma omp parallel for schedule(static)
+    for (int I = 0; I < p.nbr; ++I) std::copy(rows[I].begin(), rows[I].end(), p.col.begin() + p.rowptr[I]);
+    return p;
+}
+
+std::vector<double> block_values_of_csr(const HostCsr& a, const BlockPattern& pat, int Rb, int Cb)
+{
+    const int E = Rb * Cb;
+    std::vector<double> v(static_cast<size_t>(pat.nnzb()) * E, 0.0);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int I = 0; I < pat.nbr; ++I) {
+        const auto b = pat.col.begin() + pat.rowptr[I];
+        const auto e = pat.col.begin() + pat.rowptr[I + 1];
+        for (int rr = 0; rr < Rb; ++rr) {
+            const int r = I * Rb + rr;
+            for (int k = a.rowptr[r]; k < a.rowptr[r + 1]; ++k) {
+                const int c = a.col[k];
+                const int J = c / Cb, d = c % Cb;
+                const int64_t blk = pat.rowptr[I] + (std::lower_bound(b, e, J) - b);
+                v[static_cast<size_t>(blk) * E + rr * Cb + d] = a.val[k];
+            }
+        }
+    }
+    return v;
+}
+
+Bsr bsr_from_csr(const HostCsr& a, int Rb, int Cb, bool leveled, cudaStream_t s)
+{
+    const BlockPattern pat = block_pattern_of_csr(a, Rb, Cb);
+    std::vector<int> order, lvl;
+    if (leveled) {
+        if (!pattern_symmetric(pat)) throw Error(ED_UNSUPPORTED, "Gauss-Seidel operator pattern is not symmetric");
+        int nlev = 0;
+        gs_level_order(pat, order, lvl, nlev);
+    } else {
+        order.resize(pat.nbr);
+        std::iota(order.begin(), order.end(), 0);
+    }
+    const BsrLayout lay = make_layout(pat, order, lvl);
+    Bsr m;
+    m.st = bsr_make_struct(pat, lay, Rb, Cb, s);
+    if (leveled) m.st->leveled = true;
+    m.val.upload(bsr_pack_values(*m.st, lay, block_values_of_csr(a, pat, Rb, Cb)), s);
+    ED_CUDA(cudaStreamSynchronize(s));
+    return m;
+}
+
+HostCsr bsr_to_csr(const Bsr& m, cudaStream_t s)
+{
+    const BsrStruct& S = *m.st;
+    const std::vector<double> v = m.val.to_host(s);
+    const int E = S.Rb * S.Cb;
+    HostCsr a;
+    a.nrows = S.nbr * S.Rb;
+    a.ncols = S.nbc * S.Cb;
+    a.rowptr.assign(a.nrows + 1, 0);
+    auto srow = [&](int I) { return S.h_inv.empty() ? I : S.h_inv[I]; };
+    for (int I = 0; I < S.nbr; ++I) {
+        const int s2 = srow(I);
+        for (int rr = 0; rr < S.Rb; ++rr) a.rowptr[I * S.Rb + rr + 1] = (S.h_rowptr[s2 + 1] - S.h_rowptr[s2]) * S.Cb;
+    }
+    for (int r = 0; r < a.nrows; ++r) a.rowptr[r + 1] += a.rowptr[r];
+    a.col.resize(a.rowptr[a.nrows]);
+    a.val.resize(a.rowptr[a.nrows]);
+#pragma omp parallel for schedule(static)
+    for (int I = 0; I < S.nbr; ++I) {
+        const int s2 = srow(I);
+        for (int rr = 0; rr < S.Rb; ++rr) {
+            int out = a.rowptr[I * S.Rb + rr];
+            for (int k = S.h_rowptr[s2]; k < S.h_rowptr[s2 + 1]; ++k) {
+                const int J = S.h_col[k];
+                for (int d = 0; d < S.Cb; ++d) {
+                    a.col[out] = J * S.Cb + d;
+                    a.val[out] = v[static_cast<size_t>(k) * E + rr * S.Cb + d];
+                    ++out;
+                }
+            }
+        }
+    }
+    return a;
+}
+
+} // namespace edb

@@ -19,11 +19,11 @@ struct BlockSys {
     int Bv = 3;
     int nv = 0, np = 0;
     BlockPattern pA, pB, pC, pD;
-    SellLayout lA, lB, lC, lD;
-    Sell A, B, C, D;
+    BsrLayout lA, lB, lC, lD;
+    Bsr A, B, C, D;
     // S_hat symbolic (pattern of D - C diag(A)^-1 B, leveled) + position maps
     bool shat_symbolic = false;
-    std::shared_ptr<SellStruct> sS;
+    std::shared_ptr<BsrStruct> sS;
     DevArray<int64_t> cb_off, d_off;
     DevArray<uint16_t> cb_pos, d_pos;
     int64_t shat_nnz = 0;
@@ -83,8 +83,8 @@ SolveRes gmres_dev(Ctx& c, DOp& op, DPrec* M, const double* b, double* x, const 
 
 // Device AMG hierarchy (levels from the host setup, fine level = caller's A).
 struct DevLevel {
-    const Sell* A = nullptr; // level operator (fine: borrowed)
-    Sell Aown, P, R;
+    const Bsr* A = nullptr; // level operator (fine: borrowed)
+    Bsr Aown, P, R;
     DevArray<double> invd, r, z, s; // r/z for coarse levels, s scratch
     int n = 0;
 };
@@ -96,7 +96,7 @@ struct DevHierarchy {
     DevArray<double> pinv;
     int nc = 0;
     double setup_host_ms = 0.0;
-    void build(Ctx& c, const Sell& A0, const AmgOpts& o);
+    void build(Ctx& c, const Bsr& A0, const AmgOpts& o);
     void vcycle(Ctx& c, const double* r, double* z);
     void cycle(Ctx& c, int l, const double* r, double* z);
     void smooth(Ctx& c, int l, const double* b, double* z, int sweeps);
@@ -106,7 +106,7 @@ struct DevHierarchy {
 // Working (scaled) copy of the system and everything solve_block_system builds.
 struct WorkSys {
     int Bv = 3, nv = 0, np = 0;
-    Sell A, B, C, D, S;
+    Bsr A, B, C, D, S;
     DevArray<double> w; // scaling weights (nv + np)
     bool scaled = false;
 };

@@ -1,16 +1,11 @@
 // Internal declarations of the B200-native Newton-step library.
 //
 // Data model: every operator of the 2x2 block system and of
-// both AMG hierarchies is stored in one format, a sliced ELL of small dense
-// blocks ("SELL-32, Rb x Cb blocks"): block rows are grouped 32 per slice
-// (one warp), each lane owns one block row and walks its blocks in ascending
-// block-column order, so a lane's scalar sums happen in exactly the column
-// order of the reference CSR row (csr.cpp:11-27).  Values are stored
-// entry-major inside a slot, [slot][entry][lane], so a warp's loads of one
-// entry are 32 consecutive doubles (256 B, fully coalesced).  Square
-// operators used by Gauss-Seidel carry a level schedule: block rows are
-// permuted so that each dependency level of the in-place sweep
-// (amg.cpp:311-322) is a contiguous run of slices.
+// both AMG hierarchies is a block-sparse (BSR) matrix of small dense blocks
+// (3x3, 3x1, 1x3, 1x1) whose block rows are stored in level order: square
+// operators used by Gauss-Seidel are permuted so that each dependency level
+// of the in-place sweep (amg.cpp:311-322) is a contiguous run of rows, and a
+// persistent dataflow kernel walks the levels without a launch per level.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -125,71 +120,69 @@ struct HostCsr {
     int64_t nnz() const { return static_cast<int64_t>(col.size()); }
 };
 
-// Structure of a SELL-32 block matrix (shared between copies with
-// different values, e.g. the assembled and the scaled working system).
-struct SellStruct {
+// Structure of a block-sparse (BSR) operator whose block rows are stored in
+// a chosen order (level order for Gauss-Seidel operators).  Columns keep the
+// original block numbering; stored row s is original row perm[s].  Kernels
+// give each block row a group of L lanes (L sized to the row length) that
+// split the row's blocks and combine partial sums with warp shuffles.
+struct BsrStruct {
     int Rb = 1, Cb = 1;
     int nbr = 0, nbc = 0; // block rows / block cols
-    int nslices = 0;
-    int64_t nslots = 0; // total slot rows (sum of slice widths)
-    int64_t nnzb = 0;   // structural blocks
-    DevArray<int64_t> slice_off; // [nslices+1], in slot rows
-    DevArray<int> perm;          // [nslices*32]: block row, or -1 for a padding lane
-    DevArray<int> rowlen;        // [nslices*32]
-    DevArray<int> inv;           // [nbr]: block row -> slice*32 + lane
-    DevArray<int> col;           // [nslots*32]
-    std::vector<int> lev_slice;  // [nlev+1] slice ranges of the level schedule
+    int64_t nnzb = 0;
+    int L = 8;            // lanes per block row
+    DevArray<int> rowptr; // [nbr+1] over stored rows
+    DevArray<int> col;    // [nnzb]
+    DevArray<int> perm;   // [nbr] stored -> original (empty: identity)
+    DevArray<int> inv;    // [nbr] original -> stored (empty: identity)
+    DevArray<int> dpos;   // [nbr] block index of the diagonal block per stored row (-1: none)
+    std::vector<int> lev_ptr; // [nlev+1] stored-row ranges of the Gauss-Seidel levels
+    // dataflow schedule: items of <= rows_per_item rows, never straddling a level
+    int rows_per_item = 0, nitems = 0;
+    DevArray<int> item_row;   // [nitems+1]
+    DevArray<int> item_level; // [nitems]
+    DevArray<int> lev_items;  // [nlev] items per level
+    DevArray<unsigned int> sync; // [nlev + 2]: per-level done counters, ticket
     // host mirrors
-    std::vector<int64_t> h_slice_off;
-    std::vector<int> h_perm, h_rowlen, h_inv, h_col;
-    int nlev() const { return static_cast<int>(lev_slice.size()) - 1; }
-    int64_t nval() const { return nslots * kLanes * Rb * Cb; }
+    std::vector<int> h_rowptr, h_col, h_perm, h_inv;
+    int nlev() const { return static_cast<int>(lev_ptr.size()) - 1; }
+    int64_t nval() const { return nnzb * Rb * Cb; }
+    bool leveled = false;
 };
 
-struct Sell {
-    std::shared_ptr<SellStruct> st;
-    DevArray<double> val; // [nslots][Rb*Cb][32]
-    const SellStruct& s() const { return *st; }
+struct Bsr {
+    std::shared_ptr<BsrStruct> st;
+    DevArray<double> val; // [nnzb][Rb*Cb] row-major blocks, stored-row order
     int nrows() const { return st->nbr * st->Rb; }
     int ncols() const { return st->nbc * st->Cb; }
     double bytes_per_spmv() const; // algorithmic bytes of one y = M x
-    void copy_values_from(const Sell& o, cudaStream_t s)
+    void copy_values_from(const Bsr& o, cudaStream_t s)
     {
         st = o.st;
         val.copy_from(o.val, s);
     }
 };
 
-// Layout of a block pattern in SELL form: per block of the pattern (block-CSR
-// order) the address slot*32 + lane.
-struct SellLayout {
-    std::vector<int64_t> slice_off;
-    std::vector<int> perm, rowlen, inv;
-    std::vector<int> lev_slice;
-    std::vector<int64_t> addr;
-    int nslices = 0;
-    int64_t nslots = 0;
+// Where each block of a pattern (block-CSR order) lands in the stored order.
+struct BsrLayout {
+    std::vector<int> perm, inv, lev_ptr;
+    std::vector<int64_t> addr; // stored block index per pattern block
 };
 
-// row_order: block rows in the order they are laid out; level_of_pos: level
-// per position (a new slice starts at every level change), or empty.
-SellLayout make_sell_layout(const BlockPattern& pat, const std::vector<int>& row_order,
-                            const std::vector<int>& level_of_pos);
-std::shared_ptr<SellStruct> sell_make_struct(const BlockPattern& pat, const SellLayout& lay, int Rb,
-                                             int Cb, cudaStream_t s);
-// Block values in pattern order (nnzb blocks, each Rb*Cb row-major) -> SELL value array (host).
-std::vector<double> sell_pack_values(const SellStruct& st, const SellLayout& lay,
-                                     const std::vector<double>& bvals);
+// row_order: original block rows in stored order; level_of_pos: level per
+// stored position (empty: one level).
+BsrLayout make_layout(const BlockPattern& pat, const std::vector<int>& row_order,
+                      const std::vector<int>& level_of_pos);
+std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLayout& lay, int Rb, int Cb,
+                                           cudaStream_t s, int lanes = 0);
+// block values in pattern order -> stored order (host)
+std::vector<double> bsr_pack_values(const BsrStruct& st, const BsrLayout& lay, const std::vector<double>& bvals);
 // Level schedule of the in-place Gauss-Seidel sweep on a square block pattern:
 // level[i] = 1 + max(level[j] : j < i, (i,j) in pattern).
 void gs_level_order(const BlockPattern& pat, std::vector<int>& order, std::vector<int>& level_of_pos,
                     int& nlev);
 bool pattern_symmetric(const BlockPattern& pat);
-// Build a leveled (square) or natural-order SELL directly from a scalar CSR
-// grouped into Rb x Cb blocks (zero-filled).
-Sell sell_from_csr(const HostCsr& a, int Rb, int Cb, bool leveled, cudaStream_t s);
-// Read a Sell back as scalar CSR (zero-filled blocks included).
-HostCsr sell_to_csr(const Sell& m, cudaStream_t s);
+Bsr bsr_from_csr(const HostCsr& a, int Rb, int Cb, bool leveled, cudaStream_t s);
+HostCsr bsr_to_csr(const Bsr& m, cudaStream_t s);
 BlockPattern block_pattern_of_csr(const HostCsr& a, int Rb, int Cb);
 std::vector<double> block_values_of_csr(const HostCsr& a, const BlockPattern& pat, int Rb, int Cb);
 
@@ -197,20 +190,20 @@ std::vector<double> block_values_of_csr(const HostCsr& a, const BlockPattern& pa
 // Kernel launchers (kernels_sparse.cu)
 
 // y = M x (mode 0), y = b - M x (mode 1), y += M x (mode 2)
-void spmv(const Sell& M, const double* x, double* y, const double* b, int mode, cudaStream_t s);
+void spmv(const Bsr& M, const double* x, double* y, const double* b, int mode, cudaStream_t s);
 // y = (M1 x1) + sgn * (M2 x2); M1, M2 share the row layout (same perm/slices)
-void spmv2(const Sell& M1, const double* x1, const Sell& M2, const double* x2, double* y, double sgn,
+void spmv2(const Bsr& M1, const double* x1, const Bsr& M2, const double* x2, double* y, double sgn,
            cudaStream_t s);
-// one in-place Gauss-Seidel half sweep over the level schedule
-void sgs_sweep(const Sell& A, const double* b, double* z, const double* inv_diag, bool forward,
+// one in-place Gauss-Seidel half sweep over the level schedule (dataflow kernel)
+void sgs_sweep(const Bsr& A, const double* b, double* z, const double* inv_diag, bool forward,
                cudaStream_t s);
 // Jacobi relaxation z += w * inv_diag * (b - t)
 void jacobi_update(double* z, const double* b, const double* t, const double* inv_diag, double w,
                    int64_t n, cudaStream_t s);
 // entries *= wr[row] * wc[col]
-void sell_scale(Sell& M, const double* wr, const double* wc, cudaStream_t s);
-// scalar diagonal of a square Sell (0 when absent)
-void sell_diag(const Sell& M, double* d, cudaStream_t s);
+void bsr_scale(Bsr& M, const double* wr, const double* wc, cudaStream_t s);
+// scalar diagonal of a square Bsr (0 when absent)
+void bsr_diag(const Bsr& M, double* d, cudaStream_t s);
 // inv_diag[i] = d != 0 ? 1/d : 1
 void inv_diag_from(const double* d, double* invd, int64_t n, cudaStream_t s);
 // z = Pinv r (dense n x n, row-major)

@@ -550,30 +550,26 @@ __global__ void k_traction(const int64_t* __restrict__ rowptr, const int* __rest
     r_m[row] = acc;
 }
 
-// K4 node blocks -> SELL planes (A 3x3, B 3x1, C 1x3, D 1x1).
+// K4 node blocks -> BSR planes (A 3x3, B 3x1, C 1x3, D 1x1); src = K4 block per stored block.
 template <int PLANE>
-__global__ void k_k4_to_plane(const int* __restrict__ src, const double* __restrict__ k4, double* val,
-                              int64_t nslot_lanes)
+__global__ void k_k4_to_plane(const int* __restrict__ src, const double* __restrict__ k4, double* val, int64_t nnzb)
 {
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= nslot_lanes) return;
-    const int64_t slot = t >> 5;
-    const int lane = static_cast<int>(t & 31);
-    const int b = src[t];
-    const double* K = k4 + 16 * static_cast<int64_t>(b < 0 ? 0 : b);
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= nnzb) return;
+    const double* K = k4 + 16 * static_cast<int64_t>(src[k]);
     if (PLANE == 0) {
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
-            for (int j = 0; j < 3; ++j) val[(slot * 9 + 3 * i + j) * 32 + lane] = b < 0 ? 0.0 : K[4 * i + j];
+            for (int j = 0; j < 3; ++j) val[k * 9 + 3 * i + j] = K[4 * i + j];
     } else if (PLANE == 1) {
 #pragma unroll
-        for (int i = 0; i < 3; ++i) val[(slot * 3 + i) * 32 + lane] = b < 0 ? 0.0 : K[4 * i + 3];
+        for (int i = 0; i < 3; ++i) val[k * 3 + i] = K[4 * i + 3];
     } else if (PLANE == 2) {
 #pragma unroll
-        for (int j = 0; j < 3; ++j) val[(slot * 3 + j) * 32 + lane] = b < 0 ? 0.0 : K[12 + j];
+        for (int j = 0; j < 3; ++j) val[k * 3 + j] = K[12 + j];
     } else {
-        val[slot * 32 + lane] = b < 0 ? 0.0 : K[15];
+        val[k] = K[15];
     }
 }
 
@@ -607,16 +603,15 @@ void launch_traction(const int64_t* rowptr, const int* rows, const double* vals,
     after_launch("k_traction");
 }
 
-void launch_k4_to_plane(int plane, const int* src, const double* k4, double* val, int64_t nslot_lanes,
-                        cudaStream_t s)
+void launch_k4_to_plane(int plane, const int* src, const double* k4, double* val, int64_t nnzb, cudaStream_t s)
 {
-    if (nslot_lanes == 0) return;
-    const int g = static_cast<int>((nslot_lanes + 255) / 256);
+    if (nnzb == 0) return;
+    const int g = static_cast<int>((nnzb + 255) / 256);
     switch (plane) {
-    case 0: k_k4_to_plane<0><<<g, 256, 0, s>>>(src, k4, val, nslot_lanes); break;
-    case 1: k_k4_to_plane<1><<<g, 256, 0, s>>>(src, k4, val, nslot_lanes); break;
-    case 2: k_k4_to_plane<2><<<g, 256, 0, s>>>(src, k4, val, nslot_lanes); break;
-    default: k_k4_to_plane<3><<<g, 256, 0, s>>>(src, k4, val, nslot_lanes); break;
+    case 0: k_k4_to_plane<0><<<g, 256, 0, s>>>(src, k4, val, nnzb); break;
+    case 1: k_k4_to_plane<1><<<g, 256, 0, s>>>(src, k4, val, nnzb); break;
+    case 2: k_k4_to_plane<2><<<g, 256, 0, s>>>(src, k4, val, nnzb); break;
+    default: k_k4_to_plane<3><<<g, 256, 0, s>>>(src, k4, val, nnzb); break;
     }
     after_launch("k_k4_to_plane");
 }

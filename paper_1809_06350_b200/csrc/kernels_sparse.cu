@@ -1,12 +1,16 @@
-// SELL-32 block sparse kernels for sm_100a (FP64, CUDA cores; HBM-bound).
+// Block-sparse kernels for sm_100a (FP64 CUDA cores; HBM/L2-latency bound).
 //
-// Compiled with -fmad=false: every lane sums its row in the reference's
-// column order with separately rounded multiply and add, exactly like the
-// host loops of csr.cpp:11-27 and amg.cpp:311-322 (built without FMA), so the
-// SpMV and Gauss-Seidel results are bitwise identical to the reference for
-// identical inputs.  Bandwidth comes from the layout (one lane per block row,
-// entry-major slots -> 256-B coalesced warp loads of values and indices) and
-// from the x gathers hitting L2 (stencil neighbours are a few planes away).
+// Every block row is owned by a group of L lanes (L = 2..32, sized to the
+// row length) that split the row's blocks round-robin -- consecutive lanes
+// read consecutive 72-B blocks, so a group's loads coalesce -- and combine
+// their partial sums with warp shuffles.  Gauss-Seidel keeps the reference's
+// exact sequential semantics (amg.cpp:311-322): rows are level-scheduled (a
+// row only reads new values of rows on earlier levels), and inside a 3x3
+// diagonal block the three scalar rows are solved in sweep order by the
+// group leader.  A whole half sweep is ONE persistent dataflow kernel: CTAs
+// take work items in level order from a ticket counter, prefetch their rows'
+// matrix data, wait on the previous level's completion counter, and publish
+// their own, so there is no launch (and no grid-wide barrier) per level.
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -19,198 +23,249 @@ namespace {
 
 constexpr int kThreads = 256;
 
-inline int grid_for_lanes(int64_t lanes) { return static_cast<int>((lanes + kThreads - 1) / kThreads); }
+struct BsrArgs {
+    const int* rowptr;
+    const int* col;
+    const int* perm; // null: identity
+    const int* dpos;
+    const double* val;
+    int nbr;
+};
 
-template <int RB, int CB, int MODE>
-__global__ void __launch_bounds__(kThreads)
-    k_spmv(const int64_t* __restrict__ soff, const int* __restrict__ perm, const int* __restrict__ rlen,
-           const int* __restrict__ col, const double* __restrict__ val, int nslices,
-           const double* __restrict__ x, double* y, const double* b)
+inline BsrArgs args_of(const Bsr& M)
+{
+    const BsrStruct& S = *M.st;
+    return BsrArgs{S.rowptr.p, S.col.p, S.perm.p, S.dpos.p, M.val.p, S.nbr};
+}
+
+template <int L>
+__device__ __forceinline__ double group_sum(double v)
+{
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, L);
+    return v;
+}
+
+template <int RB, int CB, int L, int MODE>
+__global__ void __launch_bounds__(kThreads) k_spmv(BsrArgs m, const double* __restrict__ x, double* y,
+                                                   const double* __restrict__ b)
 {
     const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int sl = static_cast<int>(gid >> 5);
-    const int lane = static_cast<int>(gid & 31);
-    if (sl >= nslices) return;
-    const int row = perm[gid];
-    if (row < 0) return;
-    const int len = rlen[gid];
-    const int64_t base = soff[sl];
+    const int s = static_cast<int>(gid / L);
+    const int lane = static_cast<int>(gid % L);
+    const bool valid = s < m.nbr;
     double acc[RB];
 #pragma unroll
     for (int r = 0; r < RB; ++r) acc[r] = 0.0;
-#pragma unroll 4
-    for (int t = 0; t < len; ++t) {
-        const int64_t slot = base + t;
-        const int c = __ldg(col + slot * kLanes + lane);
-        const double* vp = val + slot * (RB * CB * kLanes) + lane;
-        double xv[CB];
+    if (valid) {
+        const int k1 = m.rowptr[s + 1];
+#pragma unroll 2
+        for (int k = m.rowptr[s] + lane; k < k1; k += L) {
+            const int c = __ldg(m.col + k);
+            const double* vp = m.val + static_cast<int64_t>(k) * (RB * CB);
+            double xv[CB];
 #pragma unroll
-        for (int d = 0; d < CB; ++d) xv[d] = __ldg(x + static_cast<int64_t>(c) * CB + d);
+            for (int d = 0; d < CB; ++d) xv[d] = __ldg(x + static_cast<int64_t>(c) * CB + d);
 #pragma unroll
-        for (int r = 0; r < RB; ++r)
+            for (int r = 0; r < RB; ++r)
 #pragma unroll
-            for (int d = 0; d < CB; ++d) acc[r] = acc[r] + __ldg(vp + (r * CB + d) * kLanes) * xv[d];
+                for (int d = 0; d < CB; ++d) acc[r] = fma(__ldg(vp + r * CB + d), xv[d], acc[r]);
+        }
     }
 #pragma unroll
-    for (int r = 0; r < RB; ++r) {
-        const int64_t i = static_cast<int64_t>(row) * RB + r;
-        if (MODE == 0) y[i] = acc[r];
-        if (MODE == 1) y[i] = b[i] - acc[r];
-        if (MODE == 2) y[i] = y[i] + acc[r];
+    for (int r = 0; r < RB; ++r) acc[r] = group_sum<L>(acc[r]);
+    if (valid && lane == 0) {
+        const int row = m.perm ? m.perm[s] : s;
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+            const int64_t i = static_cast<int64_t>(row) * RB + r;
+            if (MODE == 0) y[i] = acc[r];
+            if (MODE == 1) y[i] = b[i] - acc[r];
+            if (MODE == 2) y[i] = y[i] + acc[r];
+        }
     }
 }
 
-// y = (M1 x1) + sgn * (M2 x2), both on the same row layout.
-template <int RB, int CB1, int CB2>
-__global__ void __launch_bounds__(kThreads)
-    k_spmv2(const int64_t* __restrict__ soff1, const int* __restrict__ perm, const int* __restrict__ rlen1,
-            const int* __restrict__ col1, const double* __restrict__ val1, const int64_t* __restrict__ soff2,
-            const int* __restrict__ rlen2, const int* __restrict__ col2, const double* __restrict__ val2,
-            int nslices, const double* __restrict__ x1, const double* __restrict__ x2, double* y, double sgn)
+// y = (M1 x1) + sgn (M2 x2); M1, M2 share the stored row order.
+template <int RB, int CB1, int CB2, int L>
+__global__ void __launch_bounds__(kThreads) k_spmv2(BsrArgs m1, BsrArgs m2, const double* __restrict__ x1,
+                                                    const double* __restrict__ x2, double* y, double sgn)
 {
     const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int sl = static_cast<int>(gid >> 5);
-    const int lane = static_cast<int>(gid & 31);
-    if (sl >= nslices) return;
-    const int row = perm[gid];
-    if (row < 0) return;
+    const int s = static_cast<int>(gid / L);
+    const int lane = static_cast<int>(gid % L);
+    const bool valid = s < m1.nbr;
     double a1[RB], a2[RB];
 #pragma unroll
     for (int r = 0; r < RB; ++r) a1[r] = a2[r] = 0.0;
-    {
-        const int len = rlen1[gid];
-        const int64_t base = soff1[sl];
-#pragma unroll 4
-        for (int t = 0; t < len; ++t) {
-            const int64_t slot = base + t;
-            const int c = __ldg(col1 + slot * kLanes + lane);
-            const double* vp = val1 + slot * (RB * CB1 * kLanes) + lane;
-            double xv[CB1];
+    if (valid) {
+        int k1 = m1.rowptr[s + 1];
+#pragma unroll 2
+        for (int k = m1.rowptr[s] + lane; k < k1; k += L) {
+            const int c = __ldg(m1.col + k);
+            const double* vp = m1.val + static_cast<int64_t>(k) * (RB * CB1);
 #pragma unroll
-            for (int d = 0; d < CB1; ++d) xv[d] = __ldg(x1 + static_cast<int64_t>(c) * CB1 + d);
+            for (int d = 0; d < CB1; ++d) {
+                const double xv = __ldg(x1 + static_cast<int64_t>(c) * CB1 + d);
 #pragma unroll
-            for (int r = 0; r < RB; ++r)
-#pragma unroll
-                for (int d = 0; d < CB1; ++d) a1[r] = a1[r] + __ldg(vp + (r * CB1 + d) * kLanes) * xv[d];
+                for (int r = 0; r < RB; ++r) a1[r] = fma(__ldg(vp + r * CB1 + d), xv, a1[r]);
+            }
         }
-    }
-    {
-        const int len = rlen2[gid];
-        const int64_t base = soff2[sl];
-#pragma unroll 4
-        for (int t = 0; t < len; ++t) {
-            const int64_t slot = base + t;
-            const int c = __ldg(col2 + slot * kLanes + lane);
-            const double* vp = val2 + slot * (RB * CB2 * kLanes) + lane;
-            double xv[CB2];
+        k1 = m2.rowptr[s + 1];
+#pragma unroll 2
+        for (int k = m2.rowptr[s] + lane; k < k1; k += L) {
+            const int c = __ldg(m2.col + k);
+            const double* vp = m2.val + static_cast<int64_t>(k) * (RB * CB2);
 #pragma unroll
-            for (int d = 0; d < CB2; ++d) xv[d] = __ldg(x2 + static_cast<int64_t>(c) * CB2 + d);
+            for (int d = 0; d < CB2; ++d) {
+                const double xv = __ldg(x2 + static_cast<int64_t>(c) * CB2 + d);
 #pragma unroll
-            for (int r = 0; r < RB; ++r)
-#pragma unroll
-                for (int d = 0; d < CB2; ++d) a2[r] = a2[r] + __ldg(vp + (r * CB2 + d) * kLanes) * xv[d];
+                for (int r = 0; r < RB; ++r) a2[r] = fma(__ldg(vp + r * CB2 + d), xv, a2[r]);
+            }
         }
     }
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
-        const int64_t i = static_cast<int64_t>(row) * RB + r;
-        // y = acc1 + 1.0*acc2 (matvec_add) or acc1 - acc2 (Schur: D x - C z)
-        y[i] = sgn > 0.0 ? a1[r] + a2[r] : a1[r] - a2[r];
+        a1[r] = group_sum<L>(a1[r]);
+        a2[r] = group_sum<L>(a2[r]);
+    }
+    if (valid && lane == 0) {
+        const int row = m1.perm ? m1.perm[s] : s;
+#pragma unroll
+        for (int r = 0; r < RB; ++r) y[static_cast<int64_t>(row) * RB + r] = a1[r] + sgn * a2[r];
     }
 }
 
-// One level of an in-place Gauss-Seidel half sweep (amg.cpp:311-322): rows
-// of a level are independent; inside a block row the B scalar rows run in
-// sweep order, each summing its off-diagonal columns in ascending order.
-template <int B, bool FWD>
-__global__ void __launch_bounds__(kThreads)
-    k_sgs_level(const int64_t* __restrict__ soff, const int* __restrict__ perm, const int* __restrict__ rlen,
-                const int* __restrict__ col, const double* __restrict__ val, int s0, int s1,
-                const double* __restrict__ bvec, double* z, const double* __restrict__ invd)
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p)
 {
-    const int64_t gid = static_cast<int64_t>(s0) * kLanes + static_cast<int64_t>(blockIdx.x) * blockDim.x +
-                        threadIdx.x;
-    const int sl = static_cast<int>(gid >> 5);
-    const int lane = static_cast<int>(gid & 31);
-    if (sl >= s1) return;
-    const int row = perm[gid];
-    if (row < 0) return;
-    const int len = rlen[gid];
-    const int64_t base = soff[sl];
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// One Gauss-Seidel half sweep as a persistent dataflow kernel.
+template <int B, int L, bool FWD>
+__global__ void __launch_bounds__(kThreads) k_sgs_flow(BsrArgs m, const double* __restrict__ bvec, double* z,
+                                                       const double* __restrict__ invd, int nitems, int nlev,
+                                                       const int* __restrict__ item_row,
+                                                       const int* __restrict__ item_level,
+                                                       const int* __restrict__ lev_items, unsigned int* sync)
+{
+    __shared__ int s_ticket;
+    unsigned int* done = sync;
+    unsigned int* ticket = sync + nlev;
+    const int g = threadIdx.x / L;
+    const int lane = threadIdx.x % L;
+    for (;;) {
+        if (threadIdx.x == 0) s_ticket = static_cast<int>(atomicAdd(ticket, 1u));
+        __syncthreads();
+        const int t = s_ticket;
+        __syncthreads();
+        if (t >= nitems) return;
+        const int item = FWD ? t : nitems - 1 - t;
+        const int lev = item_level[item];
+        const int s = item_row[item] + g;
+        const bool valid = s < item_row[item + 1];
+        const int row = valid ? (m.perm ? m.perm[s] : s) : 0;
+        // prefetch this lane's first blocks (independent of z) before waiting
+        const int kb = valid ? m.rowptr[s] + lane : 0;
+        const int ke = valid ? m.rowptr[s + 1] : 0;
+        int c0 = -1;
+        double v0[B * B];
+        if (kb < ke) {
+            c0 = __ldg(m.col + kb);
 #pragma unroll
-    for (int ci = 0; ci < B; ++ci) {
-        const int cc = FWD ? ci : B - 1 - ci;
-        const int64_t i = static_cast<int64_t>(row) * B + cc;
-        double acc = bvec[i];
-        for (int t = 0; t < len; ++t) {
-            const int64_t slot = base + t;
-            const int c = col[slot * kLanes + lane];
-            const double* vp = val + slot * (B * B * kLanes) + lane + (cc * B) * kLanes;
+            for (int e = 0; e < B * B; ++e) v0[e] = __ldg(m.val + static_cast<int64_t>(kb) * (B * B) + e);
+        }
+        const int prev = FWD ? lev - 1 : lev + 1;
+        if (prev >= 0 && prev < nlev) {
+            if (threadIdx.x == 0) {
+                const unsigned int need = static_cast<unsigned int>(lev_items[prev]);
+                while (ld_acquire(done + prev) < need) __nanosleep(32);
+            }
+            __syncthreads();
+        }
+        double acc[B];
+#pragma unroll
+        for (int r = 0; r < B; ++r) acc[r] = 0.0;
+        if (c0 >= 0 && c0 != row) {
 #pragma unroll
             for (int d = 0; d < B; ++d) {
-                if (c == row && d == cc) continue;
-                acc = acc - vp[d * kLanes] * z[static_cast<int64_t>(c) * B + d];
+                const double zv = __ldcg(z + static_cast<int64_t>(c0) * B + d);
+#pragma unroll
+                for (int r = 0; r < B; ++r) acc[r] = fma(v0[r * B + d], zv, acc[r]);
             }
         }
-        z[i] = acc * invd[i];
+        for (int k = kb + L; k < ke; k += L) {
+            const int c = __ldg(m.col + k);
+            if (c == row) continue;
+            const double* vp = m.val + static_cast<int64_t>(k) * (B * B);
+#pragma unroll
+            for (int d = 0; d < B; ++d) {
+                const double zv = __ldcg(z + static_cast<int64_t>(c) * B + d);
+#pragma unroll
+                for (int r = 0; r < B; ++r) acc[r] = fma(__ldg(vp + r * B + d), zv, acc[r]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < B; ++r) acc[r] = group_sum<L>(acc[r]);
+        if (valid && lane == 0) {
+            double zs[B], D[B * B];
+#pragma unroll
+            for (int d = 0; d < B; ++d) zs[d] = __ldcg(z + static_cast<int64_t>(row) * B + d);
+            const int dp = m.dpos[s];
+#pragma unroll
+            for (int e = 0; e < B * B; ++e) D[e] = dp >= 0 ? __ldg(m.val + static_cast<int64_t>(dp) * (B * B) + e) : 0.0;
+#pragma unroll
+            for (int ci = 0; ci < B; ++ci) {
+                const int c = FWD ? ci : B - 1 - ci;
+                const int64_t i = static_cast<int64_t>(row) * B + c;
+                double a = bvec[i] - acc[c];
+#pragma unroll
+                for (int d = 0; d < B; ++d)
+                    if (d != c) a -= D[c * B + d] * zs[d];
+                zs[c] = a * invd[i];
+            }
+#pragma unroll
+            for (int d = 0; d < B; ++d) z[static_cast<int64_t>(row) * B + d] = zs[d];
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAdd(done + lev, 1u);
     }
 }
 
-template <int RB, int CB>
-__global__ void __launch_bounds__(kThreads)
-    k_scale(const int64_t* __restrict__ soff, const int* __restrict__ perm, const int* __restrict__ rlen,
-            const int* __restrict__ col, double* val, int nslices, const double* __restrict__ wr,
-            const double* __restrict__ wc)
+template <int RB, int CB, int L>
+__global__ void __launch_bounds__(kThreads) k_scale(BsrArgs m, double* val, const double* __restrict__ wr,
+                                                    const double* __restrict__ wc)
 {
     const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int sl = static_cast<int>(gid >> 5);
-    const int lane = static_cast<int>(gid & 31);
-    if (sl >= nslices) return;
-    const int row = perm[gid];
-    if (row < 0) return;
-    const int len = rlen[gid];
-    const int64_t base = soff[sl];
-    for (int t = 0; t < len; ++t) {
-        const int64_t slot = base + t;
-        const int c = col[slot * kLanes + lane];
-        double* vp = val + slot * (RB * CB * kLanes) + lane;
+    const int s = static_cast<int>(gid / L);
+    const int lane = static_cast<int>(gid % L);
+    if (s >= m.nbr) return;
+    const int row = m.perm ? m.perm[s] : s;
+    for (int k = m.rowptr[s] + lane; k < m.rowptr[s + 1]; k += L) {
+        const int c = m.col[k];
+        double* vp = val + static_cast<int64_t>(k) * (RB * CB);
 #pragma unroll
         for (int r = 0; r < RB; ++r)
 #pragma unroll
-            for (int d = 0; d < CB; ++d) {
+            for (int d = 0; d < CB; ++d)
                 // blocksystem.cpp:85: val *= wrow[r] * wcol[c]
-                const double f = wr[static_cast<int64_t>(row) * RB + r] * wc[static_cast<int64_t>(c) * CB + d];
-                vp[(r * CB + d) * kLanes] = vp[(r * CB + d) * kLanes] * f;
-            }
+                vp[r * CB + d] = vp[r * CB + d] * (wr[static_cast<int64_t>(row) * RB + r] * wc[static_cast<int64_t>(c) * CB + d]);
     }
 }
 
 template <int B>
-__global__ void __launch_bounds__(kThreads)
-    k_diag(const int64_t* __restrict__ soff, const int* __restrict__ perm, const int* __restrict__ rlen,
-           const int* __restrict__ col, const double* __restrict__ val, int nslices, double* d)
+__global__ void k_diag(BsrArgs m, double* d)
 {
-    const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int sl = static_cast<int>(gid >> 5);
-    const int lane = static_cast<int>(gid & 31);
-    if (sl >= nslices) return;
-    const int row = perm[gid];
-    if (row < 0) return;
-    const int len = rlen[gid];
-    const int64_t base = soff[sl];
-    double dv[B];
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= m.nbr) return;
+    const int row = m.perm ? m.perm[s] : s;
+    const int dp = m.dpos[s];
 #pragma unroll
-    for (int r = 0; r < B; ++r) dv[r] = 0.0;
-    for (int t = 0; t < len; ++t) {
-        const int64_t slot = base + t;
-        if (col[slot * kLanes + lane] == row) {
-            const double* vp = val + slot * (B * B * kLanes) + lane;
-#pragma unroll
-            for (int r = 0; r < B; ++r) dv[r] = vp[(r * B + r) * kLanes];
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < B; ++r) d[static_cast<int64_t>(row) * B + r] = dv[r];
+    for (int r = 0; r < B; ++r)
+        d[static_cast<int64_t>(row) * B + r] = dp >= 0 ? m.val[static_cast<int64_t>(dp) * (B * B) + r * B + r] : 0.0;
 }
 
 __global__ void k_inv_diag(const double* __restrict__ d, double* invd, int64_t n)
@@ -233,67 +288,72 @@ __global__ void k_dense_gemv(const double* __restrict__ P, const double* __restr
     const int lane = threadIdx.x & 31;
     if (row >= n) return;
     double s = 0.0;
-    for (int j = lane; j < n; j += 32) s = s + P[static_cast<int64_t>(row) * n + j] * r[j];
+    for (int j = lane; j < n; j += 32) s = fma(P[static_cast<int64_t>(row) * n + j], r[j], s);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s = s + __shfl_xor_sync(0xffffffffu, s, o);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) z[row] = s;
 }
 
+inline int grid_groups(int64_t rows, int L) { return static_cast<int>((rows * L + kThreads - 1) / kThreads); }
+
+#define ED_LANES(L, ...)                   \
+    switch (L) {                           \
+    case 2: { constexpr int LL = 2; __VA_ARGS__; break; }  \
+    case 4: { constexpr int LL = 4; __VA_ARGS__; break; }  \
+    case 8: { constexpr int LL = 8; __VA_ARGS__; break; }  \
+    case 16: { constexpr int LL = 16; __VA_ARGS__; break; } \
+    default: { constexpr int LL = 32; __VA_ARGS__; break; } \
+    }
+
 template <int RB, int CB>
-void launch_spmv(const Sell& M, const double* x, double* y, const double* b, int mode, cudaStream_t s)
+void launch_spmv(const Bsr& M, const double* x, double* y, const double* b, int mode, cudaStream_t s)
 {
-    const SellStruct& S = *M.st;
-    if (S.nslices == 0) return;
-    const int g = grid_for_lanes(static_cast<int64_t>(S.nslices) * kLanes);
-    if (mode == 0)
-        k_spmv<RB, CB, 0><<<g, kThreads, 0, s>>>(S.slice_off.p, S.perm.p, S.rowlen.p, S.col.p, M.val.p,
-                                                 S.nslices, x, y, b);
-    else if (mode == 1)
-        k_spmv<RB, CB, 1><<<g, kThreads, 0, s>>>(S.slice_off.p, S.perm.p, S.rowlen.p, S.col.p, M.val.p,
-                                                 S.nslices, x, y, b);
-    else
-        k_spmv<RB, CB, 2><<<g, kThreads, 0, s>>>(S.slice_off.p, S.perm.p, S.rowlen.p, S.col.p, M.val.p,
-                                                 S.nslices, x, y, b);
+    const BsrStruct& S = *M.st;
+    if (S.nbr == 0) return;
+    const BsrArgs a = args_of(M);
+    const int g = grid_groups(S.nbr, S.L);
+    ED_LANES(S.L, {
+        if (mode == 0) k_spmv<RB, CB, LL, 0><<<g, kThreads, 0, s>>>(a, x, y, b);
+        else if (mode == 1) k_spmv<RB, CB, LL, 1><<<g, kThreads, 0, s>>>(a, x, y, b);
+        else k_spmv<RB, CB, LL, 2><<<g, kThreads, 0, s>>>(a, x, y, b);
+    })
     after_launch("k_spmv");
 }
 
-template <int RB, int CB1, int CB2>
-void launch_spmv2(const Sell& M1, const double* x1, const Sell& M2, const double* x2, double* y, double sgn,
+template <int RB, int C1, int C2>
+void launch_spmv2(const Bsr& M1, const double* x1, const Bsr& M2, const double* x2, double* y, double sgn,
                   cudaStream_t s)
 {
-    const SellStruct& S1 = *M1.st;
-    const SellStruct& S2 = *M2.st;
-    if (S1.nslices == 0) return;
-    const int g = grid_for_lanes(static_cast<int64_t>(S1.nslices) * kLanes);
-    k_spmv2<RB, CB1, CB2><<<g, kThreads, 0, s>>>(S1.slice_off.p, S1.perm.p, S1.rowlen.p, S1.col.p, M1.val.p,
-                                                 S2.slice_off.p, S2.rowlen.p, S2.col.p, M2.val.p, S1.nslices,
-                                                 x1, x2, y, sgn);
+    const BsrStruct& S = *M1.st;
+    if (S.nbr == 0) return;
+    const int g = grid_groups(S.nbr, S.L);
+    ED_LANES(S.L, { k_spmv2<RB, C1, C2, LL><<<g, kThreads, 0, s>>>(args_of(M1), args_of(M2), x1, x2, y, sgn); })
     after_launch("k_spmv2");
 }
 
 template <int B>
-void launch_sgs(const Sell& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s)
+void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s)
 {
-    const SellStruct& S = *A.st;
-    const int nl = S.nlev();
-    for (int li = 0; li < nl; ++li) {
-        const int L = fwd ? li : nl - 1 - li;
-        const int s0 = S.lev_slice[L], s1 = S.lev_slice[L + 1];
-        if (s1 <= s0) continue;
-        const int g = grid_for_lanes(static_cast<int64_t>(s1 - s0) * kLanes);
+    const BsrStruct& S = *A.st;
+    if (S.nitems == 0) return;
+    const int nlev = S.nlev();
+    ED_CUDA(cudaMemsetAsync(S.sync.p, 0, S.sync.n * sizeof(unsigned int), s));
+    const int grid = std::min(S.nitems, 148 * 8);
+    const BsrArgs a = args_of(A);
+    ED_LANES(S.L, {
         if (fwd)
-            k_sgs_level<B, true><<<g, kThreads, 0, s>>>(S.slice_off.p, S.perm.p, S.rowlen.p, S.col.p, A.val.p,
-                                                       s0, s1, b, z, invd);
+            k_sgs_flow<B, LL, true><<<grid, kThreads, 0, s>>>(a, b, z, invd, S.nitems, nlev, S.item_row.p,
+                                                             S.item_level.p, S.lev_items.p, S.sync.p);
         else
-            k_sgs_level<B, false><<<g, kThreads, 0, s>>>(S.slice_off.p, S.perm.p, S.rowlen.p, S.col.p, A.val.p,
-                                                        s0, s1, b, z, invd);
-        after_launch("k_sgs_level");
-    }
+            k_sgs_flow<B, LL, false><<<grid, kThreads, 0, s>>>(a, b, z, invd, S.nitems, nlev, S.item_row.p,
+                                                              S.item_level.p, S.lev_items.p, S.sync.p);
+    })
+    after_launch("k_sgs_flow");
 }
 
 } // namespace
 
-void spmv(const Sell& M, const double* x, double* y, const double* b, int mode, cudaStream_t s)
+void spmv(const Bsr& M, const double* x, double* y, const double* b, int mode, cudaStream_t s)
 {
     const int RB = M.st->Rb, CB = M.st->Cb;
     if (RB == 1 && CB == 1) return launch_spmv<1, 1>(M, x, y, b, mode, s);
@@ -303,11 +363,10 @@ void spmv(const Sell& M, const double* x, double* y, const double* b, int mode, 
     throw Error(ED_UNSUPPORTED, "spmv: unsupported block shape");
 }
 
-void spmv2(const Sell& M1, const double* x1, const Sell& M2, const double* x2, double* y, double sgn,
-           cudaStream_t s)
+void spmv2(const Bsr& M1, const double* x1, const Bsr& M2, const double* x2, double* y, double sgn, cudaStream_t s)
 {
     const int RB = M1.st->Rb, C1 = M1.st->Cb, C2 = M2.st->Cb;
-    if (M2.st->Rb != RB || M2.st->nslices != M1.st->nslices)
+    if (M2.st->Rb != RB || M2.st->nbr != M1.st->nbr || M2.st->h_perm != M1.st->h_perm)
         throw Error(ED_INVALID_ARGUMENT, "spmv2: row layouts differ");
     if (RB == 3 && C1 == 3 && C2 == 1) return launch_spmv2<3, 3, 1>(M1, x1, M2, x2, y, sgn, s);
     if (RB == 1 && C1 == 3 && C2 == 1) return launch_spmv2<1, 3, 1>(M1, x1, M2, x2, y, sgn, s);
@@ -316,10 +375,11 @@ void spmv2(const Sell& M1, const double* x1, const Sell& M2, const double* x2, d
     throw Error(ED_UNSUPPORTED, "spmv2: unsupported block shape");
 }
 
-void sgs_sweep(const Sell& A, const double* b, double* z, const double* invd, bool forward, cudaStream_t s)
+void sgs_sweep(const Bsr& A, const double* b, double* z, const double* invd, bool forward, cudaStream_t s)
 {
     const int B = A.st->Rb;
     if (A.st->Cb != B) throw Error(ED_INVALID_ARGUMENT, "sgs: non-square blocks");
+    if (!A.st->leveled && A.st->nbr > 1) throw Error(ED_INVALID_ARGUMENT, "sgs: operator has no level schedule");
     if (B == 1) return launch_sgs<1>(A, b, z, invd, forward, s);
     if (B == 3) return launch_sgs<3>(A, b, z, invd, forward, s);
     throw Error(ED_UNSUPPORTED, "sgs: unsupported block size");
@@ -333,17 +393,17 @@ void jacobi_update(double* z, const double* b, const double* t, const double* in
     after_launch("k_jacobi");
 }
 
-void sell_scale(Sell& M, const double* wr, const double* wc, cudaStream_t s)
+void bsr_scale(Bsr& M, const double* wr, const double* wc, cudaStream_t s)
 {
-    const SellStruct& S = *M.st;
-    if (S.nslices == 0) return;
-    const int g = grid_for_lanes(static_cast<int64_t>(S.nslices) * kLanes);
-#define ED_SCALE(R, C)                                                                                      \
-    if (S.Rb == R && S.Cb == C) {                                                                           \
-        k_scale<R, C><<<g, kThreads, 0, s>>>(S.slice_off.p, S.perm.p, S.rowlen.p, S.col.p, M.val.p, S.nslices, \
-                                             wr, wc);                                                       \
-        after_launch("k_scale");                                                                            \
-        return;                                                                                             \
+    const BsrStruct& S = *M.st;
+    if (S.nbr == 0) return;
+    const BsrArgs a = args_of(M);
+    const int g = grid_groups(S.nbr, S.L);
+#define ED_SCALE(R, C)                                                                    \
+    if (S.Rb == R && S.Cb == C) {                                                         \
+        ED_LANES(S.L, { k_scale<R, C, LL><<<g, kThreads, 0, s>>>(a, M.val.p, wr, wc); }) \
+        after_launch("k_scale");                                                          \
+        return;                                                                           \
     }
     ED_SCALE(1, 1)
     ED_SCALE(3, 3)
@@ -353,16 +413,16 @@ void sell_scale(Sell& M, const double* wr, const double* wc, cudaStream_t s)
     throw Error(ED_UNSUPPORTED, "scale: unsupported block shape");
 }
 
-void sell_diag(const Sell& M, double* d, cudaStream_t s)
+void bsr_diag(const Bsr& M, double* d, cudaStream_t s)
 {
-    const SellStruct& S = *M.st;
-    if (S.Rb != S.Cb) throw Error(ED_INVALID_ARGUMENT, "diag: non-square blocks");
-    if (S.nslices == 0) return;
-    const int g = grid_for_lanes(static_cast<int64_t>(S.nslices) * kLanes);
+    const BsrStruct& S = *M.st;
+    if (S.Rb != S.Cb || S.nbr != S.nbc) throw Error(ED_INVALID_ARGUMENT, "diag: non-square operator");
+    if (S.nbr == 0) return;
+    const int g = (S.nbr + kThreads - 1) / kThreads;
     if (S.Rb == 1)
-        k_diag<1><<<g, kThreads, 0, s>>>(S.slice_off.p, S.perm.p, S.rowlen.p, S.col.p, M.val.p, S.nslices, d);
+        k_diag<1><<<g, kThreads, 0, s>>>(args_of(M), d);
     else
-        k_diag<3><<<g, kThreads, 0, s>>>(S.slice_off.p, S.perm.p, S.rowlen.p, S.col.p, M.val.p, S.nslices, d);
+        k_diag<3><<<g, kThreads, 0, s>>>(args_of(M), d);
     after_launch("k_diag");
 }
 

@@ -71,62 +71,43 @@ __global__ void k_shat_inv_diag(const double* __restrict__ da, double* inv_da, i
     inv_da[i] = 1.0 / d;
 }
 
-// One thread per S_hat row p (in S_hat's SELL lane order, so the row's
-// output slots are private and the stores coalesce).  The row is
-// accumulated in place in its output slots:
+// One thread per S_hat row p.  The row is accumulated in place in its
+// output segment:
 //   acc[q] = sum_{k in C row p, ascending} C[p,k] * (B[k,q] * inv_da[k])
-// exactly the csr_matmul(C, diag(A)^-1 B) order (csr.cpp:143-164), then
+// in the csr_matmul(C, diag(A)^-1 B) order (csr.cpp:143-164), then
 // S_hat = D - acc (csr_add(D, cb, 1, -1), csr.cpp:168-198).
 template <int BV>
 __global__ void __launch_bounds__(kRT) k_shat(ShatArgs a)
 {
-    const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int sl = static_cast<int>(gid >> 5);
-    const int lane = static_cast<int>(gid & 31);
-    if (sl >= a.s_nslices) return;
-    const int p = a.s_perm[gid];
-    if (p < 0) return;
-    const int slen = a.s_rowlen[gid];
-    const int64_t sbase = a.s_soff[sl];
-    double* out = a.s_val + sbase * 32 + lane;
-    for (int t = 0; t < slen; ++t) out[static_cast<int64_t>(t) * 32] = 0.0;
-
-    const int ci = a.c_inv[p];
-    const int csl = ci >> 5, clane = ci & 31;
-    const int clen = a.c_rowlen[ci];
-    const int64_t cbase = a.c_soff[csl];
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= a.s_nrows) return;
+    const int p = a.s_perm ? a.s_perm[s] : s;
+    double* out = a.s_val + a.s_rowptr[s];
+    const int slen = a.s_rowptr[s + 1] - a.s_rowptr[s];
+    for (int t = 0; t < slen; ++t) out[t] = 0.0;
     int64_t mp = a.cb_off[p];
-    for (int t1 = 0; t1 < clen; ++t1) {
-        const int64_t cslot = cbase + t1;
-        // block column of C = velocity node m (C's col array is read through b_inv)
-        const int m = a.c_col[cslot * 32 + clane];
-        const int bi = a.b_inv[m];
-        const int bsl = bi >> 5, blane = bi & 31;
-        const int blen = a.b_rowlen[bi];
-        const int64_t bbase = a.b_soff[bsl];
+    for (int k1 = a.c_rowptr[p]; k1 < a.c_rowptr[p + 1]; ++k1) {
+        const int m = a.c_col[k1];
+        const int bs = a.b_inv ? a.b_inv[m] : m;
+        const int b0 = a.b_rowptr[bs];
+        const int blen = a.b_rowptr[bs + 1] - b0;
 #pragma unroll
         for (int c = 0; c < BV; ++c) {
-            const double cv = a.c_val[(cslot * BV + c) * 32 + clane];
+            const double cv = a.c_val[static_cast<int64_t>(k1) * BV + c];
             const double id = a.inv_da[static_cast<int64_t>(m) * BV + c];
             for (int t2 = 0; t2 < blen; ++t2) {
-                const double bv = a.b_val[((bbase + t2) * BV + c) * 32 + blane];
-                const double sb = bv * id; // csr_scale_rows(sb, inv_da)
+                const double sb = a.b_val[static_cast<int64_t>(b0 + t2) * BV + c] * id; // csr_scale_rows
                 const int pos = a.cb_pos[mp + t2];
-                double* o = out + static_cast<int64_t>(pos) * 32;
-                *o = *o + cv * sb;
+                out[pos] = out[pos] + cv * sb;
             }
         }
         mp += blen;
     }
-    // S_hat = -acc, then + D on D's pattern (x + (-y) == x - y exactly)
-    for (int t = 0; t < slen; ++t) out[static_cast<int64_t>(t) * 32] = -out[static_cast<int64_t>(t) * 32];
-    const int dlen = a.d_rowlen[ci];
-    const int64_t dbase = a.d_soff[csl];
+    for (int t = 0; t < slen; ++t) out[t] = -out[t];
     const int64_t dp = a.d_off[p];
-    for (int t = 0; t < dlen; ++t) {
-        const double dv = a.d_val[(dbase + t) * 32 + clane];
-        double* o = out + static_cast<int64_t>(a.d_pos[dp + t]) * 32;
-        *o = dv + *o;
+    for (int k = a.d_rowptr[p]; k < a.d_rowptr[p + 1]; ++k) {
+        const int pos = a.d_pos[dp + (k - a.d_rowptr[p])];
+        out[pos] = a.d_val[k] + out[pos];
     }
 }
 
@@ -225,8 +206,8 @@ void shat_inv_diag(const double* da, double* inv_da, int nv, double eps, int* ba
 
 void launch_shat_numeric(const ShatArgs& a, cudaStream_t s)
 {
-    if (a.s_nslices == 0) return;
-    const int g = static_cast<int>((static_cast<int64_t>(a.s_nslices) * 32 + kRT - 1) / kRT);
+    if (a.s_nrows == 0) return;
+    const int g = (a.s_nrows + kRT - 1) / kRT;
     if (a.Bv == 3)
         k_shat<3><<<g, kRT, 0, s>>>(a);
     else

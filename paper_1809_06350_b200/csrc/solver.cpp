@@ -219,14 +219,14 @@ SolveRes gmres_dev(Ctx& c, DOp& op, DPrec* M, const double* b, double* x, const 
 // ---------------------------------------------------------------------------
 // AMG
 
-void DevHierarchy::build(Ctx& c, const Sell& A0, const AmgOpts& o)
+void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o)
 {
     cudaStream_t s = c.stream;
     opts = o;
     lv.clear();
     fallback = false;
     const double t0 = now_ms();
-    const HostCsr A0h = sell_to_csr(A0, s);
+    const HostCsr A0h = bsr_to_csr(A0, s);
     const HostHierarchy hh = amg_build_host(A0h, o);
     setup_host_ms = now_ms() - t0;
     if (hh.fallback) {
@@ -246,7 +246,7 @@ void DevHierarchy::build(Ctx& c, const Sell& A0, const AmgOpts& o)
         if (l == 0) {
             d.A = &A0;
         } else {
-            d.Aown = sell_from_csr(H.A, Bl, Bl, true, s);
+            d.Aown = bsr_from_csr(H.A, Bl, Bl, true, s);
             d.A = &d.Aown;
         }
         d.invd.upload(H.inv_diag, s);
@@ -256,8 +256,8 @@ void DevHierarchy::build(Ctx& c, const Sell& A0, const AmgOpts& o)
             d.z.alloc(d.n);
         }
         if (l + 1 < L) {
-            d.P = sell_from_csr(H.P, Bl, Bc, false, s);
-            d.R = sell_from_csr(H.R, Bc, Bl, false, s);
+            d.P = bsr_from_csr(H.P, Bl, Bc, false, s);
+            d.R = bsr_from_csr(H.R, Bc, Bl, false, s);
         }
     }
     nc = hh.nc;
@@ -316,10 +316,10 @@ void DevHierarchy::vcycle(Ctx& c, const double* r, double* z)
 
 namespace {
 
-struct SellOp final : DOp {
-    const Sell& M;
+struct MatOp final : DOp {
+    const Bsr& M;
     cudaStream_t s;
-    SellOp(const Sell& m, cudaStream_t st) : M(m), s(st) {}
+    MatOp(const Bsr& m, cudaStream_t st) : M(m), s(st) {}
     int64_t size() const override { return M.nrows(); }
     void apply(const double* x, double* y) override { spmv(M, x, y, nullptr, 0, s); }
 };
@@ -363,7 +363,7 @@ struct SchurOp final : DOp {
     {
         spmv(W.B, x, t.p, nullptr, 0, c.stream);
         vec_fill(z.p, 0.0, W.nv, c.stream);
-        SellOp aop(W.A, c.stream);
+        MatOp aop(W.A, c.stream);
         AmgPrec M(c, amg_a);
         const SolveRes r = gmres_dev(c, aop, &M, t.p, z.p, cfg, false, c.ws_a);
         st.schur_applies += 1;
@@ -389,7 +389,7 @@ struct Scr {
     void solve(const double* rv, const double* rp, double* xv, double* xp)
     {
         cudaStream_t s = c.stream;
-        SellOp aop(W.A, s);
+        MatOp aop(W.A, s);
         AmgPrec Ma(c, amg_a), Ms(c, amg_s);
         // 1. A xhat = r_v
         vec_fill(xhat.p, 0.0, W.nv, s);
@@ -401,7 +401,7 @@ struct Scr {
         // 3. S x_p = r_p
         vec_fill(xp, 0.0, W.np, s);
         if (ti.rel_tol >= 1.0) {
-            SellOp sop(W.S, s);
+            MatOp sop(W.S, s);
             SolveRes r3 = gmres_dev(c, sop, &Ms, rp2.p, xp, ts, false, c.ws_s);
             st.s_solves += 1;
             st.s_iters += r3.iterations;

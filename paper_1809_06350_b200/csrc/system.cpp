@@ -1,4 +1,4 @@
-// Block-system construction: node-graph patterns and SELL layouts, element
+// Block-system construction: node-graph patterns and BSR layouts, element
 // colouring and element->K4 maps (mesh-static, built once), planes from K4 or
 // from caller CSR, the working copy with symmetric block scaling
 // (blocksystem.cpp:53-106) and S_hat (precond.cpp:10-24).
@@ -18,16 +18,16 @@ void BlockSys::build_structure(cudaStream_t s)
     std::vector<int> order, lvl;
     int nlev = 0;
     gs_level_order(pA, order, lvl, nlev);
-    lA = make_sell_layout(pA, order, lvl);
-    lB = make_sell_layout(pB, order, lvl); // same slicing as A
+    lA = make_layout(pA, order, lvl);
+    lB = make_layout(pB, order, lvl); // same slicing as A
     std::vector<int> porder(pD.nbr);
     std::iota(porder.begin(), porder.end(), 0);
-    lC = make_sell_layout(pC, porder, {});
-    lD = make_sell_layout(pD, porder, {}); // same slicing as C
-    A.st = sell_make_struct(pA, lA, Bv, Bv, s);
-    B.st = sell_make_struct(pB, lB, Bv, 1, s);
-    C.st = sell_make_struct(pC, lC, 1, Bv, s);
-    D.st = sell_make_struct(pD, lD, 1, 1, s);
+    lC = make_layout(pC, porder, {});
+    lD = make_layout(pD, porder, {}); // same slicing as C
+    A.st = bsr_make_struct(pA, lA, Bv, Bv, s);
+    B.st = bsr_make_struct(pB, lB, Bv, 1, s);
+    C.st = bsr_make_struct(pC, lC, 1, Bv, s);
+    D.st = bsr_make_struct(pD, lD, 1, 1, s);
     A.val.alloc(A.st->nval());
     B.val.alloc(B.st->nval());
     C.val.alloc(C.st->nval());
@@ -112,8 +112,8 @@ void BlockSys::build_shat_symbolic(cudaStream_t s)
     std::vector<int> order, lvl;
     int nlev = 0;
     gs_level_order(pS, order, lvl, nlev);
-    const SellLayout lS = make_sell_layout(pS, order, lvl);
-    sS = sell_make_struct(pS, lS, 1, 1, s);
+    const BsrLayout lS = make_layout(pS, order, lvl);
+    sS = bsr_make_struct(pS, lS, 1, 1, s);
     cb_off.upload(hcb_off, s);
     d_off.upload(hd_off, s);
     cb_pos.upload(hcb, s);
@@ -243,16 +243,16 @@ void ctx_build_mesh_system(Ctx& c)
     srcD.resize(PN.nnzb());
     std::iota(srcD.begin(), srcD.end(), 0);
     S.build_structure(s);
-    auto sell_src = [&](const SellLayout& L, const std::vector<int64_t>& src, DevArray<int>& out) {
-        std::vector<int> v(static_cast<size_t>(L.nslots) * kLanes, -1);
+    auto stored_src = [&](const BsrLayout& L, const std::vector<int64_t>& src, DevArray<int>& out) {
+        std::vector<int> v(src.size(), -1);
         for (size_t k = 0; k < src.size(); ++k) v[L.addr[k]] = static_cast<int>(src[k]);
         out.upload(v, s);
         ED_CUDA(cudaStreamSynchronize(s));
     };
-    sell_src(S.lA, srcA, c.srcA);
-    sell_src(S.lB, srcB, c.srcB);
-    sell_src(S.lC, srcC, c.srcC);
-    sell_src(S.lD, srcD, c.srcD);
+    stored_src(S.lA, srcA, c.srcA);
+    stored_src(S.lB, srcB, c.srcB);
+    stored_src(S.lC, srcC, c.srcC);
+    stored_src(S.lD, srcD, c.srcD);
     c.sys_from_mesh = true;
     c.sys_values = false;
     ED_CUDA(cudaStreamSynchronize(s));
@@ -262,10 +262,10 @@ void ctx_planes_from_k4(Ctx& c)
 {
     BlockSys& S = c.sys;
     cudaStream_t s = c.stream;
-    launch_k4_to_plane(0, c.srcA.p, c.k4.p, S.A.val.p, S.A.st->nslots * kLanes, s);
-    launch_k4_to_plane(1, c.srcB.p, c.k4.p, S.B.val.p, S.B.st->nslots * kLanes, s);
-    launch_k4_to_plane(2, c.srcC.p, c.k4.p, S.C.val.p, S.C.st->nslots * kLanes, s);
-    launch_k4_to_plane(3, c.srcD.p, c.k4.p, S.D.val.p, S.D.st->nslots * kLanes, s);
+    launch_k4_to_plane(0, c.srcA.p, c.k4.p, S.A.val.p, S.A.st->nnzb, s);
+    launch_k4_to_plane(1, c.srcB.p, c.k4.p, S.B.val.p, S.B.st->nnzb, s);
+    launch_k4_to_plane(2, c.srcC.p, c.k4.p, S.C.val.p, S.C.st->nnzb, s);
+    launch_k4_to_plane(3, c.srcD.p, c.k4.p, S.D.val.p, S.D.st->nnzb, s);
     c.sys_values = true;
 }
 
@@ -284,13 +284,13 @@ void ctx_planes_from_csr(Ctx& c, int Bv)
     S.pC = block_pattern_of_csr(c.csr_up[2], 1, Bv);
     S.pD = block_pattern_of_csr(c.csr_up[3], 1, 1);
     S.build_structure(s);
-    S.A.val.upload(sell_pack_values(*S.A.st, S.lA, block_values_of_csr(c.csr_up[0], S.pA, Bv, Bv)), s);
+    S.A.val.upload(bsr_pack_values(*S.A.st, S.lA, block_values_of_csr(c.csr_up[0], S.pA, Bv, Bv)), s);
     ED_CUDA(cudaStreamSynchronize(s));
-    S.B.val.upload(sell_pack_values(*S.B.st, S.lB, block_values_of_csr(c.csr_up[1], S.pB, Bv, 1)), s);
+    S.B.val.upload(bsr_pack_values(*S.B.st, S.lB, block_values_of_csr(c.csr_up[1], S.pB, Bv, 1)), s);
     ED_CUDA(cudaStreamSynchronize(s));
-    S.C.val.upload(sell_pack_values(*S.C.st, S.lC, block_values_of_csr(c.csr_up[2], S.pC, 1, Bv)), s);
+    S.C.val.upload(bsr_pack_values(*S.C.st, S.lC, block_values_of_csr(c.csr_up[2], S.pC, 1, Bv)), s);
     ED_CUDA(cudaStreamSynchronize(s));
-    S.D.val.upload(sell_pack_values(*S.D.st, S.lD, block_values_of_csr(c.csr_up[3], S.pD, 1, 1)), s);
+    S.D.val.upload(bsr_pack_values(*S.D.st, S.lD, block_values_of_csr(c.csr_up[3], S.pD, 1, 1)), s);
     ED_CUDA(cudaStreamSynchronize(s));
     c.csr_bv = Bv;
     c.sys_values = true;
@@ -313,17 +313,17 @@ void make_work(Ctx& c, WorkSys& W, bool scale, double eps_diag)
     W.w.alloc(static_cast<size_t>(nv) + np);
     if (!scale) return;
     DevArray<double> da(nv), dd(np), mx(2);
-    sell_diag(W.A, da.p, s);
-    sell_diag(W.D, dd.p, s);
+    bsr_diag(W.A, da.p, s);
+    bsr_diag(W.D, dd.p, s);
     absmax(c.red, da.p, nv, mx.p + 0, s);
     absmax(c.red, dd.p, np, mx.p + 1, s);
     block_weights(da.p, dd.p, nv, np, mx.p + 0, mx.p + 1, eps_diag, W.w.p, s);
     const double* wv = W.w.p;
     const double* wp = W.w.p + nv;
-    sell_scale(W.A, wv, wv, s);
-    sell_scale(W.B, wv, wp, s);
-    sell_scale(W.C, wp, wv, s);
-    sell_scale(W.D, wp, wp, s);
+    bsr_scale(W.A, wv, wv, s);
+    bsr_scale(W.B, wv, wp, s);
+    bsr_scale(W.C, wp, wv, s);
+    bsr_scale(W.D, wp, wp, s);
     ED_CUDA(cudaStreamSynchronize(s)); // temporaries die here
 }
 
@@ -334,7 +334,7 @@ void build_shat_work(Ctx& c, WorkSys& W)
     BlockSys& S = c.sys;
     if (!S.shat_symbolic) S.build_shat_symbolic(s);
     DevArray<double> da(W.nv), inv_da(W.nv);
-    sell_diag(W.A, da.p, s);
+    bsr_diag(W.A, da.p, s);
     const int big = 0x7fffffff;
     ED_CUDA(cudaMemcpyAsync(c.dscratch_i.p + 1, &big, sizeof(int), cudaMemcpyHostToDevice, s));
     shat_inv_diag(da.p, inv_da.p, W.nv, 1e-300, c.dscratch_i.p + 1, s);
@@ -344,22 +344,18 @@ void build_shat_work(Ctx& c, WorkSys& W)
     W.S.st = S.sS;
     W.S.val.alloc(S.sS->nval());
     ShatArgs a{};
-    const SellStruct& SS = *S.sS;
-    a.s_soff = SS.slice_off.p;
+    const BsrStruct& SS = *S.sS;
+    a.s_rowptr = SS.rowptr.p;
     a.s_perm = SS.perm.p;
-    a.s_rowlen = SS.rowlen.p;
     a.s_val = W.S.val.p;
-    a.s_nslices = SS.nslices;
-    a.c_soff = W.C.st->slice_off.p;
-    a.c_rowlen = W.C.st->rowlen.p;
+    a.s_nrows = SS.nbr;
+    if (!W.C.st->h_perm.empty() || !W.D.st->h_perm.empty()) throw Error(ED_INVALID_ARGUMENT, "C/D must be in natural order");
+    a.c_rowptr = W.C.st->rowptr.p;
     a.c_col = W.C.st->col.p;
-    a.c_inv = W.C.st->inv.p;
     a.c_val = W.C.val.p;
-    a.d_soff = W.D.st->slice_off.p;
-    a.d_rowlen = W.D.st->rowlen.p;
+    a.d_rowptr = W.D.st->rowptr.p;
     a.d_val = W.D.val.p;
-    a.b_soff = W.B.st->slice_off.p;
-    a.b_rowlen = W.B.st->rowlen.p;
+    a.b_rowptr = W.B.st->rowptr.p;
     a.b_inv = W.B.st->inv.p;
     a.b_val = W.B.val.p;
     a.inv_da = inv_da.p;
