@@ -204,27 +204,27 @@ std::vector<std::vector<int>> strong_neighbors(const HostCsr& A, const std::vect
 #pragma omp parallel
     {
         std::vector<int> touched;
-        std::vector<double> acc;
+        std::vector<double> acc(n_nodes, 0.0);
+        std::vector<char> seen(n_nodes, 0);
 #pragma omp for schedule(dynamic, 512)
         for (int I = 0; I < n_nodes; ++I) {
             touched.clear();
-            acc.clear();
             for (int r = nstart[I]; r < nstart[I + 1]; ++r)
                 for (int k = A.rowptr[r]; k < A.rowptr[r + 1]; ++k) {
                     const int J = node_of_row[A.col[k]];
                     if (J == I) continue;
-                    size_t t = 0;
-                    while (t < touched.size() && touched[t] != J) ++t;
-                    if (t == touched.size()) {
+                    if (!seen[J]) {
+                        seen[J] = 1;
                         touched.push_back(J);
-                        acc.push_back(0.0);
                     }
-                    acc[t] += A.val[k] * A.val[k];
+                    acc[J] += A.val[k] * A.val[k];
                 }
-            for (size_t t = 0; t < touched.size(); ++t) {
-                const int J = touched[t];
-                const double s2 = acc[t];
+            for (const int J : touched) {
+                const double s2 = acc[J];
+                acc[J] = 0.0;
+                seen[J] = 0;
                 if (diag_w[I] <= 0.0 || diag_w[J] <= 0.0) continue;
+                // diag_w holds squared Frobenius norms, hence the quarter power
                 if (std::sqrt(s2) > theta * std::pow(diag_w[I] * diag_w[J], 0.25)) nbr[I].push_back(J);
             }
         }

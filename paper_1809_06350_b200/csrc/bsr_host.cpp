@@ -141,6 +141,11 @@ std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLay
     S.lev_items.upload(lcnt, s);
     S.sync.alloc(static_cast<size_t>(std::max(nlev, 1)) + 2);
     S.sync.zero(s);
+    S.d_lev_ptr.upload(S.lev_ptr, s);
+    // narrow level schedules (every level fits one 512-thread CTA in <= 2 passes) run as one CTA
+    int widest = 0;
+    for (int l = 0; l < nlev; ++l) widest = std::max(widest, S.lev_ptr[l + 1] - S.lev_ptr[l]);
+    S.chain = static_cast<int64_t>(widest) * S.L <= 1024;
     ED_CUDA(cudaStreamSynchronize(s)); // host vectors die at return
     return st;
 }

@@ -142,6 +142,8 @@ struct BsrStruct {
     DevArray<int> item_level; // [nitems]
     DevArray<int> lev_items;  // [nlev] items per level
     DevArray<unsigned int> sync; // [nlev + 2]: per-level done counters, ticket
+    bool chain = false;          // narrow levels: single-CTA sweep with CTA barriers
+    DevArray<int> d_lev_ptr;     // device copy of lev_ptr
     // host mirrors
     std::vector<int> h_rowptr, h_col, h_perm, h_inv;
     int nlev() const { return static_cast<int>(lev_ptr.size()) - 1; }

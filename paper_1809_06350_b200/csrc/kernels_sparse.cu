@@ -143,7 +143,100 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p)
     return v;
 }
 
-// One Gauss-Seidel half sweep as a persistent dataflow kernel.
+// Row work of one Gauss-Seidel update (amg.cpp:311-322) for stored row s
+// by a group of L lanes.  Everything that does not depend on z (the lane's
+// first PF blocks, b, inv_diag, the diagonal block, the row's own old z) is
+// loaded by prefetch_row() BEFORE the dependency wait; finish_row() then only
+// gathers off-diagonal z values.
+template <int B, int PF>
+struct RowPref {
+    int row, kb, ke;
+    int c[PF];
+    double v[PF][B * B];
+    double b[B], id[B], D[B * B], zs[B];
+};
+
+template <int B, int L, int PF>
+__device__ __forceinline__ void prefetch_row(const BsrArgs& m, const double* __restrict__ bvec,
+                                             const double* __restrict__ invd, const double* z, int s, bool valid,
+                                             int lane, RowPref<B, PF>& P)
+{
+    P.row = valid ? (m.perm ? m.perm[s] : s) : 0;
+    P.kb = valid ? m.rowptr[s] + lane : 0;
+    P.ke = valid ? m.rowptr[s + 1] : 0;
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+        const int k = P.kb + q * L;
+        P.c[q] = k < P.ke ? __ldg(m.col + k) : -1;
+        if (k < P.ke) {
+#pragma unroll
+            for (int e = 0; e < B * B; ++e) P.v[q][e] = __ldg(m.val + static_cast<int64_t>(k) * (B * B) + e);
+        }
+    }
+    if (valid && lane == 0) {
+        const int dp = m.dpos[s];
+#pragma unroll
+        for (int d = 0; d < B; ++d) {
+            const int64_t i = static_cast<int64_t>(P.row) * B + d;
+            P.b[d] = bvec[i];
+            P.id[d] = invd[i];
+            P.zs[d] = __ldcg(z + i); // only this row's owner writes z[row]
+        }
+#pragma unroll
+        for (int e = 0; e < B * B; ++e) P.D[e] = dp >= 0 ? __ldg(m.val + static_cast<int64_t>(dp) * (B * B) + e) : 0.0;
+    }
+}
+
+template <int B, int L, int PF, bool FWD, bool CG>
+__device__ __forceinline__ void finish_row(const BsrArgs& m, double* z, bool valid, int lane, const RowPref<B, PF>& P)
+{
+    double acc[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) acc[r] = 0.0;
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+        const int c = P.c[q];
+        if (c >= 0 && c != P.row) {
+#pragma unroll
+            for (int d = 0; d < B; ++d) {
+                const double zv = CG ? __ldcg(z + static_cast<int64_t>(c) * B + d) : z[static_cast<int64_t>(c) * B + d];
+#pragma unroll
+                for (int r = 0; r < B; ++r) acc[r] = fma(P.v[q][r * B + d], zv, acc[r]);
+            }
+        }
+    }
+    for (int k = P.kb + PF * L; k < P.ke; k += L) {
+        const int c = __ldg(m.col + k);
+        if (c == P.row) continue;
+        const double* vp = m.val + static_cast<int64_t>(k) * (B * B);
+#pragma unroll
+        for (int d = 0; d < B; ++d) {
+            const double zv = CG ? __ldcg(z + static_cast<int64_t>(c) * B + d) : z[static_cast<int64_t>(c) * B + d];
+#pragma unroll
+            for (int r = 0; r < B; ++r) acc[r] = fma(__ldg(vp + r * B + d), zv, acc[r]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < B; ++r) acc[r] = group_sum<L>(acc[r]);
+    if (valid && lane == 0) {
+        double zs[B];
+#pragma unroll
+        for (int d = 0; d < B; ++d) zs[d] = P.zs[d];
+#pragma unroll
+        for (int ci = 0; ci < B; ++ci) {
+            const int c = FWD ? ci : B - 1 - ci;
+            double a = P.b[c] - acc[c];
+#pragma unroll
+            for (int d = 0; d < B; ++d)
+                if (d != c) a -= P.D[c * B + d] * zs[d];
+            zs[c] = a * P.id[c];
+        }
+#pragma unroll
+        for (int d = 0; d < B; ++d) z[static_cast<int64_t>(P.row) * B + d] = zs[d];
+    }
+}
+
+// One Gauss-Seidel half sweep over wide levels: persistent dataflow kernel.
 template <int B, int L, bool FWD>
 __global__ void __launch_bounds__(kThreads) k_sgs_flow(BsrArgs m, const double* __restrict__ bvec, double* z,
                                                        const double* __restrict__ invd, int nitems, int nlev,
@@ -151,6 +244,7 @@ __global__ void __launch_bounds__(kThreads) k_sgs_flow(BsrArgs m, const double* 
                                                        const int* __restrict__ item_level,
                                                        const int* __restrict__ lev_items, unsigned int* sync)
 {
+    constexpr int PF = (B == 3) ? 2 : 4;
     __shared__ int s_ticket;
     unsigned int* done = sync;
     unsigned int* ticket = sync + nlev;
@@ -166,72 +260,47 @@ __global__ void __launch_bounds__(kThreads) k_sgs_flow(BsrArgs m, const double* 
         const int lev = item_level[item];
         const int s = item_row[item] + g;
         const bool valid = s < item_row[item + 1];
-        const int row = valid ? (m.perm ? m.perm[s] : s) : 0;
-        // prefetch this lane's first blocks (independent of z) before waiting
-        const int kb = valid ? m.rowptr[s] + lane : 0;
-        const int ke = valid ? m.rowptr[s + 1] : 0;
-        int c0 = -1;
-        double v0[B * B];
-        if (kb < ke) {
-            c0 = __ldg(m.col + kb);
-#pragma unroll
-            for (int e = 0; e < B * B; ++e) v0[e] = __ldg(m.val + static_cast<int64_t>(kb) * (B * B) + e);
-        }
+        RowPref<B, PF> P;
+        prefetch_row<B, L, PF>(m, bvec, invd, z, s, valid, lane, P);
         const int prev = FWD ? lev - 1 : lev + 1;
         if (prev >= 0 && prev < nlev) {
             if (threadIdx.x == 0) {
                 const unsigned int need = static_cast<unsigned int>(lev_items[prev]);
-                while (ld_acquire(done + prev) < need) __nanosleep(32);
+                while (ld_acquire(done + prev) < need) __nanosleep(20);
             }
             __syncthreads();
         }
-        double acc[B];
-#pragma unroll
-        for (int r = 0; r < B; ++r) acc[r] = 0.0;
-        if (c0 >= 0 && c0 != row) {
-#pragma unroll
-            for (int d = 0; d < B; ++d) {
-                const double zv = __ldcg(z + static_cast<int64_t>(c0) * B + d);
-#pragma unroll
-                for (int r = 0; r < B; ++r) acc[r] = fma(v0[r * B + d], zv, acc[r]);
-            }
-        }
-        for (int k = kb + L; k < ke; k += L) {
-            const int c = __ldg(m.col + k);
-            if (c == row) continue;
-            const double* vp = m.val + static_cast<int64_t>(k) * (B * B);
-#pragma unroll
-            for (int d = 0; d < B; ++d) {
-                const double zv = __ldcg(z + static_cast<int64_t>(c) * B + d);
-#pragma unroll
-                for (int r = 0; r < B; ++r) acc[r] = fma(__ldg(vp + r * B + d), zv, acc[r]);
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < B; ++r) acc[r] = group_sum<L>(acc[r]);
-        if (valid && lane == 0) {
-            double zs[B], D[B * B];
-#pragma unroll
-            for (int d = 0; d < B; ++d) zs[d] = __ldcg(z + static_cast<int64_t>(row) * B + d);
-            const int dp = m.dpos[s];
-#pragma unroll
-            for (int e = 0; e < B * B; ++e) D[e] = dp >= 0 ? __ldg(m.val + static_cast<int64_t>(dp) * (B * B) + e) : 0.0;
-#pragma unroll
-            for (int ci = 0; ci < B; ++ci) {
-                const int c = FWD ? ci : B - 1 - ci;
-                const int64_t i = static_cast<int64_t>(row) * B + c;
-                double a = bvec[i] - acc[c];
-#pragma unroll
-                for (int d = 0; d < B; ++d)
-                    if (d != c) a -= D[c * B + d] * zs[d];
-                zs[c] = a * invd[i];
-            }
-#pragma unroll
-            for (int d = 0; d < B; ++d) z[static_cast<int64_t>(row) * B + d] = zs[d];
-        }
-        __threadfence();
+        finish_row<B, L, PF, FWD, true>(m, z, valid, lane, P);
         __syncthreads();
-        if (threadIdx.x == 0) atomicAdd(done + lev, 1u);
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(done + lev, 1u);
+        }
+    }
+}
+
+// One Gauss-Seidel half sweep over narrow levels: a single CTA walks the
+// levels with a CTA barrier between them (no global atomics or polling).
+template <int B, int L, bool FWD>
+__global__ void __launch_bounds__(512) k_sgs_chain(BsrArgs m, const double* __restrict__ bvec, double* z,
+                                                    const double* __restrict__ invd, const int* __restrict__ lev_ptr,
+                                                    int nlev)
+{
+    constexpr int PF = (B == 3) ? 2 : 4;
+    constexpr int G = 512 / L;
+    const int g = threadIdx.x / L;
+    const int lane = threadIdx.x % L;
+    for (int li = 0; li < nlev; ++li) {
+        const int lev = FWD ? li : nlev - 1 - li;
+        const int r0 = lev_ptr[lev], r1 = lev_ptr[lev + 1];
+        for (int base = r0; base < r1; base += G) {
+            const int s = base + g;
+            const bool valid = s < r1;
+            RowPref<B, PF> P;
+            prefetch_row<B, L, PF>(m, bvec, invd, z, s, valid, lane, P);
+            finish_row<B, L, PF, FWD, false>(m, z, valid, lane, P);
+        }
+        __syncthreads();
     }
 }
 
@@ -337,9 +406,19 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
     const BsrStruct& S = *A.st;
     if (S.nitems == 0) return;
     const int nlev = S.nlev();
-    ED_CUDA(cudaMemsetAsync(S.sync.p, 0, S.sync.n * sizeof(unsigned int), s));
-    const int grid = std::min(S.nitems, 148 * 8);
     const BsrArgs a = args_of(A);
+    if (S.chain) {
+        ED_LANES(S.L, {
+            if (fwd)
+                k_sgs_chain<B, LL, true><<<1, 512, 0, s>>>(a, b, z, invd, S.d_lev_ptr.p, nlev);
+            else
+                k_sgs_chain<B, LL, false><<<1, 512, 0, s>>>(a, b, z, invd, S.d_lev_ptr.p, nlev);
+        })
+        after_launch("k_sgs_chain");
+        return;
+    }
+    ED_CUDA(cudaMemsetAsync(S.sync.p, 0, S.sync.n * sizeof(unsigned int), s));
+    const int grid = std::min(S.nitems, 148 * 2);
     ED_LANES(S.L, {
         if (fwd)
             k_sgs_flow<B, LL, true><<<grid, kThreads, 0, s>>>(a, b, z, invd, S.nitems, nlev, S.item_row.p,

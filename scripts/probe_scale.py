@@ -11,7 +11,7 @@ for n in [int(a) for a in sys.argv[1:]] or [40]:
     st = cp.seeded_state()
     ctx.set_state(st)
     opts = cp.solver_options()
-    for rep in range(2):
+    for rep in range(int(os.environ.get("REPS", "2"))):
         t = time.time(); out = ctx.newton_first_pass(cp.ts, opts); t_pass = time.time() - t
         ctx.set_state(st)
         print(json.dumps(dict(n=n, nu=nu, rep=rep, mesh_s=round(t_mesh, 2), ctx_s=round(t_ctx, 2), pass_s=round(t_pass, 3),
