@@ -210,6 +210,18 @@ int ed_shat_export(ed_ctx* ctx, const ed_block_solver_options* opts, int32_t* di
 int ed_block_matvec_device(ed_ctx* ctx, const double* d_x, double* d_y, int n_rep, float* ms);
 /* Bytes moved per coupled SpMV / per A-plane SpMV (algorithmic). */
 int ed_spmv_bytes(ed_ctx* ctx, double* coupled_bytes, double* a_plane_bytes);
+/* Keep / restore a device-side copy of the state (benchmark steps restart
+ * from the same y_n without host traffic). */
+int ed_state_save(ed_ctx* ctx);
+int ed_state_restore(ed_ctx* ctx);
+/* CUDA events on the context's stream: op 0 records the start event, op 1
+ * records the stop event, synchronises and returns the elapsed ms. */
+int ed_timer(ed_ctx* ctx, int op, float* ms);
+/* Device-timed hot kernels on the current (solver-scaled) system, n_rep
+ * launches each.  out[2k] = average ms per launch, out[2k+1] = algorithmic
+ * bytes per launch, for k = 0 coupled K x, 1 A-plane SpMV, 2 fine-level
+ * Gauss-Seidel forward sweep on A, 3 S_hat SpMV. */
+int ed_bench_kernels(ed_ctx* ctx, const ed_block_solver_options* opts, int n_rep, double* out);
 
 #ifdef __cplusplus
 }

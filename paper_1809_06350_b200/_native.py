@@ -26,7 +26,8 @@ EXPORTED = [
     "ed_state_download", "ed_assemble_residuals", "ed_assemble_tangent", "ed_tangent_export",
     "ed_foldin_download", "ed_block_system_upload", "ed_solve_block_system",
     "ed_solve_block_system_device", "ed_newton_first_pass", "ed_block_matvec", "ed_gmres_a",
-    "ed_amg_vcycle", "ed_shat_export", "ed_block_matvec_device", "ed_spmv_bytes",
+    "ed_amg_vcycle", "ed_shat_export", "ed_block_matvec_device", "ed_spmv_bytes", "ed_state_save",
+    "ed_state_restore", "ed_timer", "ed_bench_kernels",
 ]
 
 
@@ -132,6 +133,10 @@ def lib():
         "ed_shat_export": (C.c_int, [P, C.POINTER(BlockSolverOptions), ip, ip, ip, dp]),
         "ed_block_matvec_device": (C.c_int, [P, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_float)]),
         "ed_spmv_bytes": (C.c_int, [P, dp, dp]),
+        "ed_state_save": (C.c_int, [P]),
+        "ed_state_restore": (C.c_int, [P]),
+        "ed_timer": (C.c_int, [P, C.c_int, C.POINTER(C.c_float)]),
+        "ed_bench_kernels": (C.c_int, [P, C.POINTER(BlockSolverOptions), C.c_int, dp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -355,6 +355,28 @@ class Context:
                                                        C.byref(opts), C.byref(st), N.dp(h), hist_cap, C.byref(hl)))
         return st.as_dict(), h[: hl.value].copy()
 
+    def state_save(self):
+        self._chk(N.lib().ed_state_save(self._p))
+
+    def state_restore(self):
+        self._chk(N.lib().ed_state_restore(self._p))
+
+    def timer_start(self):
+        self._chk(N.lib().ed_timer(self._p, 0, None))
+
+    def timer_stop(self) -> float:
+        ms = C.c_float()
+        self._chk(N.lib().ed_timer(self._p, 1, C.byref(ms)))
+        return ms.value
+
+    def bench_kernels(self, opts=None, n_rep=10):
+        """Device-timed hot kernels: {name: (ms per launch, algorithmic bytes)}."""
+        opts = opts or block_solver_options()
+        out = np.zeros(8)
+        self._chk(N.lib().ed_bench_kernels(self._p, C.byref(opts), n_rep, N.dp(out)))
+        names = ("coupled_spmv", "a_spmv", "sgs_fwd_fine", "shat_spmv")
+        return {k: (float(out[2 * i]), float(out[2 * i + 1])) for i, k in enumerate(names)}
+
     @staticmethod
     def kernel_launches():
         return int(N.lib().ed_kernel_launches(None))

@@ -44,10 +44,10 @@ HostCsr csr_matmul(const HostCsr& a, const HostCsr& b)
         std::vector<int> marker(b.ncols, -1);
 #pragma omp for schedule(dynamic, 1024)
         for (int r = 0; r < a.nrows; ++r) {
-            int cnt = 0;
-            for (int ka = a.rowptr[r]; ka < a.rowptr[r + 1]; ++ka) {
+            int64_t cnt = 0;
+            for (int64_t ka = a.rowptr[r]; ka < a.rowptr[r + 1]; ++ka) {
                 const int k = a.col[ka];
-                for (int kb = b.rowptr[k]; kb < b.rowptr[k + 1]; ++kb) {
+                for (int64_t kb = b.rowptr[k]; kb < b.rowptr[k + 1]; ++kb) {
                     const int j = b.col[kb];
                     if (marker[j] != r) {
                         marker[j] = r;
@@ -69,10 +69,10 @@ HostCsr csr_matmul(const HostCsr& a, const HostCsr& b)
 #pragma omp for schedule(dynamic, 1024)
         for (int r = 0; r < a.nrows; ++r) {
             row_cols.clear();
-            for (int ka = a.rowptr[r]; ka < a.rowptr[r + 1]; ++ka) {
+            for (int64_t ka = a.rowptr[r]; ka < a.rowptr[r + 1]; ++ka) {
                 const int k = a.col[ka];
                 const double av = a.val[ka];
-                for (int kb = b.rowptr[k]; kb < b.rowptr[k + 1]; ++kb) {
+                for (int64_t kb = b.rowptr[k]; kb < b.rowptr[k + 1]; ++kb) {
                     const int j = b.col[kb];
                     if (marker[j] != r) {
                         marker[j] = r;
@@ -83,7 +83,7 @@ HostCsr csr_matmul(const HostCsr& a, const HostCsr& b)
                 }
             }
             std::sort(row_cols.begin(), row_cols.end());
-            int out = c.rowptr[r];
+            int64_t out = c.rowptr[r];
             for (const int j : row_cols) {
                 c.col[out] = j;
                 c.val[out] = acc[j];
@@ -105,10 +105,10 @@ HostCsr csr_transpose(const HostCsr& a)
     for (int r = 0; r < t.nrows; ++r) t.rowptr[r + 1] += t.rowptr[r];
     t.col.resize(a.col.size());
     t.val.resize(a.val.size());
-    std::vector<int> next(t.rowptr.begin(), t.rowptr.end() - 1);
+    std::vector<int64_t> next(t.rowptr.begin(), t.rowptr.end() - 1);
     for (int r = 0; r < a.nrows; ++r)
-        for (int k = a.rowptr[r]; k < a.rowptr[r + 1]; ++k) {
-            const int pos = next[a.col[k]]++;
+        for (int64_t k = a.rowptr[r]; k < a.rowptr[r + 1]; ++k) {
+            const int64_t pos = next[a.col[k]]++;
             t.col[pos] = r;
             t.val[pos] = a.val[k];
         }
@@ -125,8 +125,8 @@ HostCsr csr_add(const HostCsr& a, const HostCsr& b, double alpha, double beta)
     c.rowptr.assign(a.nrows + 1, 0);
 #pragma omp parallel for schedule(static)
     for (int r = 0; r < a.nrows; ++r) {
-        int ka = a.rowptr[r], kb = b.rowptr[r], cnt = 0;
-        const int ea = a.rowptr[r + 1], eb = b.rowptr[r + 1];
+        int64_t ka = a.rowptr[r], kb = b.rowptr[r], cnt = 0;
+        const int64_t ea = a.rowptr[r + 1], eb = b.rowptr[r + 1];
         while (ka < ea || kb < eb) {
             if (kb >= eb || (ka < ea && a.col[ka] < b.col[kb]))
                 ++ka;
@@ -145,8 +145,8 @@ HostCsr csr_add(const HostCsr& a, const HostCsr& b, double alpha, double beta)
     c.val.resize(c.rowptr[a.nrows]);
 #pragma omp parallel for schedule(static)
     for (int r = 0; r < a.nrows; ++r) {
-        int ka = a.rowptr[r], kb = b.rowptr[r], out = c.rowptr[r];
-        const int ea = a.rowptr[r + 1], eb = b.rowptr[r + 1];
+        int64_t ka = a.rowptr[r], kb = b.rowptr[r], out = c.rowptr[r];
+        const int64_t ea = a.rowptr[r + 1], eb = b.rowptr[r + 1];
         while (ka < ea || kb < eb) {
             int j;
             double v;
@@ -175,7 +175,7 @@ void matvec(const HostCsr& a, const double* x, double* y) // csr.cpp:11-18
 #pragma omp parallel for schedule(static)
     for (int r = 0; r < a.nrows; ++r) {
         double s = 0.0;
-        for (int k = a.rowptr[r]; k < a.rowptr[r + 1]; ++k) s += a.val[k] * x[a.col[k]];
+        for (int64_t k = a.rowptr[r]; k < a.rowptr[r + 1]; ++k) s += a.val[k] * x[a.col[k]];
         y[r] = s;
     }
 }
@@ -198,7 +198,7 @@ std::vector<std::vector<int>> strong_neighbors(const HostCsr& A, const std::vect
 #pragma omp parallel for schedule(static)
     for (int I = 0; I < n_nodes; ++I)
         for (int r = nstart[I]; r < nstart[I + 1]; ++r)
-            for (int k = A.rowptr[r]; k < A.rowptr[r + 1]; ++k)
+            for (int64_t k = A.rowptr[r]; k < A.rowptr[r + 1]; ++k)
                 if (node_of_row[A.col[k]] == I) diag_w[I] += A.val[k] * A.val[k];
     std::vector<std::vector<int>> nbr(n_nodes);
 #pragma omp parallel
@@ -210,7 +210,7 @@ std::vector<std::vector<int>> strong_neighbors(const HostCsr& A, const std::vect
         for (int I = 0; I < n_nodes; ++I) {
             touched.clear();
             for (int r = nstart[I]; r < nstart[I + 1]; ++r)
-                for (int k = A.rowptr[r]; k < A.rowptr[r + 1]; ++k) {
+                for (int64_t k = A.rowptr[r]; k < A.rowptr[r + 1]; ++k) {
                     const int J = node_of_row[A.col[k]];
                     if (J == I) continue;
                     if (!seen[J]) {
@@ -334,7 +334,7 @@ HostCsr tentative_prolongator(int nrows, int k, const std::vector<int>& agg_of_r
     P.ncols = n_agg * k;
     P.rowptr.assign(nrows + 1, 0);
     for (int r = 0; r < nrows; ++r) {
-        int cnt = 0;
+        int64_t cnt = 0;
         for (int c = 0; c < k; ++c) cnt += Qrow[static_cast<size_t>(r) * k + c] != 0.0;
         P.rowptr[r + 1] = P.rowptr[r] + cnt;
     }
@@ -342,7 +342,7 @@ HostCsr tentative_prolongator(int nrows, int k, const std::vector<int>& agg_of_r
     P.val.resize(P.rowptr[nrows]);
 #pragma omp parallel for schedule(static)
     for (int r = 0; r < nrows; ++r) {
-        int out = P.rowptr[r];
+        int64_t out = P.rowptr[r];
         for (int c = 0; c < k; ++c) {
             const double q = Qrow[static_cast<size_t>(r) * k + c];
             if (q != 0.0) {
@@ -619,7 +619,7 @@ HostHierarchy amg_build_host(const HostCsr& A0, const AmgOpts& opts)
             T.lap("AP_tent", lvl, AP.nrows, AP.nnz());
 #pragma omp parallel for schedule(static)
             for (int r = 0; r < AP.nrows; ++r)
-                for (int kk = AP.rowptr[r]; kk < AP.rowptr[r + 1]; ++kk) AP.val[kk] *= lv.inv_diag[r];
+                for (int64_t kk = AP.rowptr[r]; kk < AP.rowptr[r + 1]; ++kk) AP.val[kk] *= lv.inv_diag[r];
             P = csr_add(P, AP, 1.0, -omega);
             T.lap("smooth_P", lvl, P.nrows, P.nnz());
         }
@@ -652,7 +652,7 @@ HostHierarchy amg_build_host(const HostCsr& A0, const AmgOpts& opts)
     h.nc = Ac.nrows;
     std::vector<double> dense(static_cast<size_t>(Ac.nrows) * Ac.ncols, 0.0);
     for (int r = 0; r < Ac.nrows; ++r)
-        for (int kk = Ac.rowptr[r]; kk < Ac.rowptr[r + 1]; ++kk)
+        for (int64_t kk = Ac.rowptr[r]; kk < Ac.rowptr[r + 1]; ++kk)
             dense[static_cast<size_t>(Ac.col[kk]) * Ac.nrows + r] = Ac.val[kk];
     h.pinv = cod_pinv(dense, Ac.nrows, 1e-12);
     T.lap("coarse_cod", static_cast<int>(h.levels.size()) - 1, Ac.nrows, Ac.nnz());

@@ -67,6 +67,8 @@ Ctx::Ctx(int dev) : device(dev)
 Ctx::~Ctx()
 {
     cudaStreamSynchronize(stream);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
     if (pinned) cudaFreeHost(pinned);
     if (stream) cudaStreamDestroy(stream);
 }
@@ -459,7 +461,7 @@ int ed_tangent_export(ed_ctx* ctx, int which, int32_t* dims, int32_t* rowptr, in
             dims[2] = static_cast<int32_t>(a.nnz());
         }
         if (rowptr) {
-            std::copy(a.rowptr.begin(), a.rowptr.end(), rowptr);
+            for (size_t i = 0; i < a.rowptr.size(); ++i) rowptr[i] = static_cast<int32_t>(a.rowptr[i]);
             std::copy(a.col.begin(), a.col.end(), col);
             std::copy(a.val.begin(), a.val.end(), val);
         }
@@ -492,7 +494,7 @@ int ed_block_system_upload(ed_ctx* ctx, int nv, int np, const int32_t* a_rp, con
             m.col.assign(cc, cc + nnz);
             m.val.assign(vv, vv + nnz);
             for (int r = 0; r < nr; ++r)
-                for (int k = m.rowptr[r]; k < m.rowptr[r + 1]; ++k) {
+                for (int64_t k = m.rowptr[r]; k < m.rowptr[r + 1]; ++k) {
                     if (m.col[k] < 0 || m.col[k] >= nc) throw Error(ED_INVALID_ARGUMENT, "column out of range");
                     if (k > m.rowptr[r] && m.col[k] <= m.col[k - 1])
                         throw Error(ED_INVALID_ARGUMENT, "columns must be sorted and unique");
@@ -785,10 +787,104 @@ int ed_shat_export(ed_ctx* ctx, const ed_block_solver_options* opts, int32_t* di
             dims[2] = static_cast<int32_t>(a.nnz());
         }
         if (rowptr) {
-            std::copy(a.rowptr.begin(), a.rowptr.end(), rowptr);
+            for (size_t i = 0; i < a.rowptr.size(); ++i) rowptr[i] = static_cast<int32_t>(a.rowptr[i]);
             std::copy(a.col.begin(), a.col.end(), col);
             std::copy(a.val.begin(), a.val.end(), val);
         }
+    });
+}
+
+int ed_state_save(ed_ctx* ctx)
+{
+    return guarded(ctx, [&](Ctx& c) {
+        check(c.have_dofs, ED_NOT_READY, "dofs required");
+        c.s_u.copy_from(c.u, c.stream);
+        c.s_udot.copy_from(c.udot, c.stream);
+        c.s_p.copy_from(c.p, c.stream);
+        c.s_pdot.copy_from(c.pdot, c.stream);
+        c.s_v.copy_from(c.v, c.stream);
+        c.s_vdot.copy_from(c.vdot, c.stream);
+        c.sync();
+    });
+}
+
+int ed_state_restore(ed_ctx* ctx)
+{
+    return guarded(ctx, [&](Ctx& c) {
+        check(c.s_u.n == c.u.n && c.s_u.p, ED_NOT_READY, "no saved state");
+        c.u.copy_from(c.s_u, c.stream);
+        c.udot.copy_from(c.s_udot, c.stream);
+        c.p.copy_from(c.s_p, c.stream);
+        c.pdot.copy_from(c.s_pdot, c.stream);
+        c.v.copy_from(c.s_v, c.stream);
+        c.vdot.copy_from(c.s_vdot, c.stream);
+    });
+}
+
+int ed_timer(ed_ctx* ctx, int op, float* ms)
+{
+    return guarded(ctx, [&](Ctx& c) {
+        if (!c.ev0) {
+            ED_CUDA(cudaEventCreate(&c.ev0));
+            ED_CUDA(cudaEventCreate(&c.ev1));
+        }
+        if (op == 0) {
+            ED_CUDA(cudaEventRecord(c.ev0, c.stream));
+        } else {
+            ED_CUDA(cudaEventRecord(c.ev1, c.stream));
+            ED_CUDA(cudaEventSynchronize(c.ev1));
+            float t = 0.0f;
+            ED_CUDA(cudaEventElapsedTime(&t, c.ev0, c.ev1));
+            if (ms) *ms = t;
+        }
+    });
+}
+
+int ed_bench_kernels(ed_ctx* ctx, const ed_block_solver_options* opts, int n_rep, double* out)
+{
+    return guarded(ctx, [&](Ctx& c) {
+        check(opts && out && n_rep > 0, ED_INVALID_ARGUMENT, "bad arguments");
+        ensure_system(c, opts);
+        WorkSys& W = c.work;
+        make_work(c, W, opts->scale != 0, opts->eps_diag);
+        build_shat_work(c, W);
+        const int64_t n = static_cast<int64_t>(W.nv) + W.np;
+        DevArray<double> x(n), y(n), invd(W.nv), d(W.nv);
+        vec_fill(x.p, 1.0, n, c.stream);
+        vec_fill(y.p, 0.0, n, c.stream);
+        bsr_diag(W.A, d.p, c.stream);
+        inv_diag_from(d.p, invd.p, W.nv, c.stream);
+        cudaEvent_t e0, e1;
+        ED_CUDA(cudaEventCreate(&e0));
+        ED_CUDA(cudaEventCreate(&e1));
+        auto time = [&](auto&& f) {
+            f(); // warm
+            ED_CUDA(cudaEventRecord(e0, c.stream));
+            for (int r = 0; r < n_rep; ++r) f();
+            ED_CUDA(cudaEventRecord(e1, c.stream));
+            ED_CUDA(cudaEventSynchronize(e1));
+            float t = 0.0f;
+            ED_CUDA(cudaEventElapsedTime(&t, e0, e1));
+            return static_cast<double>(t) / n_rep;
+        };
+        const int nv = W.nv;
+        out[0] = time([&] {
+            spmv2(W.A, x.p, W.B, x.p + nv, y.p, 1.0, c.stream);
+            spmv2(W.C, x.p, W.D, x.p + nv, y.p + nv, 1.0, c.stream);
+        });
+        const BlockSys& S = c.sys;
+        out[1] = S.A.st->nnzb * (8.0 * S.Bv * S.Bv + 4.0) + S.B.st->nnzb * (8.0 * S.Bv + 4.0) +
+                 S.C.st->nnzb * (8.0 * S.Bv + 4.0) + S.D.st->nnzb * 12.0 +
+                 2.0 * 8.0 * (static_cast<double>(S.nv) + S.np) + 4.0 * (S.A.st->nbr + S.C.st->nbr + 2);
+        out[2] = time([&] { spmv(W.A, x.p, y.p, nullptr, 0, c.stream); });
+        out[3] = W.A.bytes_per_spmv();
+        out[4] = time([&] { sgs_sweep(W.A, x.p, y.p, invd.p, true, c.stream); });
+        // values+indices once, plus b and inv_diag read, z read+written
+        out[5] = W.A.st->nnzb * (8.0 * W.Bv * W.Bv + 4.0) + 4.0 * (W.A.st->nbr + 1) + 4.0 * 8.0 * nv;
+        out[6] = time([&] { spmv(W.S, x.p, y.p, nullptr, 0, c.stream); });
+        out[7] = W.S.bytes_per_spmv();
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
     });
 }
 

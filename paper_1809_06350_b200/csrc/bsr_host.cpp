@@ -176,7 +176,7 @@ BlockPattern block_pattern_of_csr(const HostCsr& a, int Rb, int Cb)
         for (int I = 0; I < p.nbr; ++I) {
             auto& cols = rows[I];
             for (int r = I * Rb; r < (I + 1) * Rb; ++r)
-                for (int k = a.rowptr[r]; k < a.rowptr[r + 1]; ++k) {
+                for (int64_t k = a.rowptr[r]; k < a.rowptr[r + 1]; ++k) {
                     const int J = a.col[k] / Cb;
                     if (mark[J] != I) {
                         mark[J] = I;
@@ -203,7 +203,7 @@ std::vector<double> block_values_of_csr(const HostCsr& a, const BlockPattern& pa
         const auto e = pat.col.begin() + pat.rowptr[I + 1];
         for (int rr = 0; rr < Rb; ++rr) {
             const int r = I * Rb + rr;
-            for (int k = a.rowptr[r]; k < a.rowptr[r + 1]; ++k) {
+            for (int64_t k = a.rowptr[r]; k < a.rowptr[r + 1]; ++k) {
                 const int c = a.col[k];
                 const int J = c / Cb, d = c % Cb;
                 const int64_t blk = pat.rowptr[I] + (std::lower_bound(b, e, J) - b);
@@ -247,7 +247,8 @@ HostCsr bsr_to_csr(const Bsr& m, cudaStream_t s)
     auto srow = [&](int I) { return S.h_inv.empty() ? I : S.h_inv[I]; };
     for (int I = 0; I < S.nbr; ++I) {
         const int s2 = srow(I);
-        for (int rr = 0; rr < S.Rb; ++rr) a.rowptr[I * S.Rb + rr + 1] = (S.h_rowptr[s2 + 1] - S.h_rowptr[s2]) * S.Cb;
+        for (int rr = 0; rr < S.Rb; ++rr)
+            a.rowptr[I * S.Rb + rr + 1] = static_cast<int64_t>(S.h_rowptr[s2 + 1] - S.h_rowptr[s2]) * S.Cb;
     }
     for (int r = 0; r < a.nrows; ++r) a.rowptr[r + 1] += a.rowptr[r];
     a.col.resize(a.rowptr[a.nrows]);
@@ -256,7 +257,7 @@ HostCsr bsr_to_csr(const Bsr& m, cudaStream_t s)
     for (int I = 0; I < S.nbr; ++I) {
         const int s2 = srow(I);
         for (int rr = 0; rr < S.Rb; ++rr) {
-            int out = a.rowptr[I * S.Rb + rr];
+            int64_t out = a.rowptr[I * S.Rb + rr];
             for (int k = S.h_rowptr[s2]; k < S.h_rowptr[s2 + 1]; ++k) {
                 const int J = S.h_col[k];
                 for (int d = 0; d < S.Cb; ++d) {

@@ -143,6 +143,8 @@ struct Ctx {
     DevArray<double> u, udot, p, pdot, v, vdot;
     DevArray<double> m_u, m_udot, m_p, m_pdot, m_v, m_vdot; // stage state
     DevArray<double> rm, rp, fv, fp, rk, rhs, xsol;
+    DevArray<double> s_u, s_udot, s_p, s_pdot, s_v, s_vdot; // saved state (benchmarks)
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     DevArray<int> dscratch_i; // [0] bad element, [1] bad row
     // system
     BlockSys sys;                 // assembled or uploaded (unscaled)

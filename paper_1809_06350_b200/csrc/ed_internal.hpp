@@ -115,7 +115,8 @@ struct BlockPattern {
 // Host-side scalar CSR (mirror of CsrMatrix, csr.hpp:13-46).
 struct HostCsr {
     int nrows = 0, ncols = 0;
-    std::vector<int> rowptr, col;
+    std::vector<int64_t> rowptr;
+    std::vector<int> col;
     std::vector<double> val;
     int64_t nnz() const { return static_cast<int64_t>(col.size()); }
 };

@@ -6,7 +6,8 @@ from paper_1809_06350_b200 import CubeProblem
 
 for n in [int(a) for a in sys.argv[1:]] or [40]:
     nu = 0.5 if n in (40, 160) else 0.45
-    t = time.time(); cp = CubeProblem(n=n, nu=nu); t_mesh = time.time() - t
+    dt = float(os.environ.get("DT", "1e-3"))
+    t = time.time(); cp = CubeProblem(n=n, nu=nu, dt=dt); t_mesh = time.time() - t
     t = time.time(); ctx = cp.context(0); t_ctx = time.time() - t
     st = cp.seeded_state()
     ctx.set_state(st)
