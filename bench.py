@@ -1,0 +1,262 @@
+#!/usr/bin/env python
+"""Newton-step benchmark for the B200 hot path (BASELINE.json metric:
+"Newton linear solves/s and BSR SpMV GB/s vs HBM peak (160^3 cube)").
+
+One *step* = one first corrector pass of step_generalized_alpha
+(timeint.cpp:54-176) on the seeded 160^3 cube (configs[4]): predictor,
+stage blend, residual assembly, tangent assembly with the kinematic fold-in,
+solve_block_system with the nested (SCR) preconditioner -- including both
+AMG hierarchy setups -- and the two-stage update.  Every step restarts from
+the same seeded state (device-side copy), so K steps are K identical Newton
+linear solves.  Inputs (matrix planes, ~10 GB) are far larger than L2, so no
+explicit L2 flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU: the path does not shard (exact Gauss-Seidel and greedy
+aggregation are global-order dependent) -> N independent
+replicas, one process per GPU, value = total solves / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Newton linear solves/s and BSR SpMV GB/s vs HBM peak (160^3 cube, 16.5M dofs)"
+UNIT = "solves/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=160, help="cells per cube edge (configs[4]: 160)")
+    ap.add_argument("--nu", type=float, default=0.5)
+    ap.add_argument("--dt", type=float, default=0.1)
+    ap.add_argument("--cpu-sample-n", type=int, default=16, help="cube size of the bounded CPU sample")
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy test)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi clock/throttle sampling during the timed region."""
+
+    def __init__(self, device):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+        return world, rank, local, dist
+    return 1, 0, 0, None
+
+
+def max_over_ranks(dist, value):
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def cpu_reference_step(n, nu, dt):
+    """The reference CPU path (oracle/_ref, single-threaded like the
+    reference) on one seeded cube: one first corrector pass."""
+    from oracle import ref
+    from paper_1809_06350_b200 import CubeProblem
+
+    cp = CubeProblem(n=n, nu=nu, dt=dt)
+    P = ref.RefProblem(ref.cube_params(n, nu=nu, dt=dt))
+    st = cp.seeded_state()
+    opts = ref.SolverOptions.from_buffer_copy(bytes(cp.solver_options()))
+    P.set_state(st.u, st.udot, st.p, st.pdot, st.v, st.vdot)
+    t0 = time.perf_counter()
+    out = P.newton_first_pass(opts)
+    return time.perf_counter() - t0, out, cp
+
+
+def run_reference(args, world, rank, dist):
+    if rank != 0:
+        return
+    n = args.cpu_sample_n
+    for _ in range(args.warmup):
+        cpu_reference_step(n, args.nu, args.dt)
+    times = []
+    for _ in range(args.steps):
+        t, out, cp = cpu_reference_step(n, args.nu, args.dt)
+        times.append(t)
+    tot = sum(times)
+    value = args.steps / tot
+    sample = (f"reference first corrector pass on the {n}^3 cube ({cp.nv + cp.np} unknowns, seeded, nu={args.nu}, "
+              f"dt={args.dt}); the 160^3 reference needs ~230 GB host RAM and hours (SURVEY.md §8d)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64 state)",
+        "config": {"workload": f"cube {n}^3 first Newton corrector pass (bounded CPU sample of configs[4])",
+                   "n": n, "nu": args.nu, "dt": args.dt},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_ours(args, world, rank, local, dist):
+    import numpy as np
+
+    from paper_1809_06350_b200 import CubeProblem
+
+    cp = CubeProblem(n=args.n, nu=args.nu, dt=args.dt)
+    st = cp.seeded_state()
+    ctx = cp.context(local)
+    opts = cp.solver_options()
+    ctx.set_state(st)
+    ctx.state_save()
+    # warm-up (builds every mesh-static structure: patterns, S_hat symbolic, level schedules)
+    for _ in range(args.warmup):
+        ctx.state_restore()
+        out = ctx.newton_first_pass(cp.ts, opts)
+    barrier(dist)
+    clocks = Clocks(local)
+    l0 = ctx.kernel_launches()
+    ctx.timer_start()
+    phase = []
+    for _ in range(args.steps):
+        ctx.state_restore()
+        out = ctx.newton_first_pass(cp.ts, opts)
+        phase.append(out["times"])
+    ms = ctx.timer_stop()
+    launches = ctx.kernel_launches() - l0
+    clk = clocks.stop()
+    ms_max = max_over_ranks(dist, ms)
+    barrier(dist)
+    value = world * args.steps / (ms_max / 1e3)
+
+    # end to end through the public API: host state in, solution out
+    h2d = 14 * 8 * cp.mesh.n_nodes
+    d2h = 8 * (cp.nv + cp.np) + 8
+    e2e_ms = []
+    for _ in range(args.e2e_steps):
+        barrier(dist)
+        t0 = time.perf_counter()
+        ctx.set_state(st)
+        out_e = ctx.newton_first_pass(cp.ts, opts)
+        e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    e2e_max = max_over_ranks(dist, max(e2e_ms))
+    e2e_value = world / (e2e_max / 1e3)
+
+    kern = ctx.bench_kernels(opts, n_rep=10)
+    if rank != 0:
+        return
+    peak, peak_src = peaks()
+    # dominant device kernel by bytes x launches: the coupled SpMV is the
+    # metric's named kernel; report it as the headline roofline and the rest
+    # beside it
+    rl = {}
+    for name, (kms, kbytes) in kern.items():
+        gbs = kbytes / (kms * 1e-3) / 1e9
+        rl[name] = {"ms": kms, "bytes": kbytes, "achieved_gbs": gbs, "frac": gbs / peak}
+    head = rl["coupled_spmv"]
+    cpu = None
+    if world == 1:
+        t_cpu, _, cpc = cpu_reference_step(args.cpu_sample_n, args.nu, args.dt)
+        cpu = {"value": 1.0 / t_cpu, "unit": UNIT, "cores": 1, "kind": "reference",
+               "sample": f"reference (oracle/_ref, 1 thread) first corrector pass on the {args.cpu_sample_n}^3 cube "
+                         f"({cpc.nv + cpc.np} unknowns) in {t_cpu:.2f} s; the full 160^3 reference needs ~230 GB "
+                         f"host RAM (SURVEY.md §8d)"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64 state, SURVEY.md §8d)",
+        "config": {"workload": f"cube {args.n}^3 first Newton corrector pass (configs[4])", "n": args.n,
+                   "nu": args.nu, "dt": args.dt, "unknowns": cp.nv + cp.np, "tets": cp.mesh.n_tets,
+                   "parallelism": f"replicas{world}", "l2_flush": "inputs > L2 (matrix planes ~10 GB)",
+                   "solver": "FGMRES(200) 1e-6 / SCR a,s,inner 1e-2, AMG SGS (reference defaults)"},
+        "roofline": {"bound": "hbm", "kernel": "coupled 4x4 BSR SpMV K x", "achieved": head["achieved_gbs"],
+                     "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": head["frac"],
+                     "traffic": None, "kernels": rl},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "newton": {"norm": out["norm"], "stats": out["stats"], "phase_ms_last": phase[-1] if phase else None},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local, dist = dist_init(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank, dist)
+    else:
+        run_ours(args, world, rank, local, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
