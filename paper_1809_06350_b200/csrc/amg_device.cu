@@ -1,0 +1,834 @@
+// Smoothed-aggregation AMG setup on the GPU; see amg_device.hpp.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <numeric>
+
+#include "amg_device.hpp"
+
+namespace edb {
+
+namespace {
+
+constexpr int kT = 256;
+
+inline int g1(int64_t n) { return static_cast<int>(std::max<int64_t>(1, (n + kT - 1) / kT)); }
+
+struct Timer {
+    bool on = std::getenv("ED_AMG_VERBOSE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void lap(cudaStream_t s, const char* what, int lvl, long a, long b)
+    {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[amg-dev] L%d %-12s %9.3f s  %ld %ld\n", lvl, what,
+                     std::chrono::duration<double>(now - t).count(), a, b);
+        t = now;
+    }
+};
+
+// ---- natural-order copy of a (level-permuted) Bsr -------------------------
+__global__ void k_rowlen_nat(const int* __restrict__ rowptr, const int* __restrict__ inv, int n, int* len)
+{
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= n) return;
+    const int s = inv ? inv[I] : I;
+    len[I] = rowptr[s + 1] - rowptr[s];
+}
+
+__global__ void k_copy_rows(const int* __restrict__ rp_in, const int* __restrict__ col_in,
+                            const double* __restrict__ val_in, const int* __restrict__ inv, int n, int E,
+                            const int* __restrict__ rp_out, int* col_out, double* val_out)
+{
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= n) return;
+    const int s = inv ? inv[I] : I;
+    const int k0 = rp_in[s], k1 = rp_in[s + 1], o = rp_out[I];
+    for (int k = k0; k < k1; ++k) {
+        col_out[o + k - k0] = col_in[k];
+        for (int e = 0; e < E; ++e) val_out[static_cast<int64_t>(o + k - k0) * E + e] = val_in[static_cast<int64_t>(k) * E + e];
+    }
+}
+
+// ---- strength graph (amg.cpp:32-81) ---------------------------------------
+template <int B>
+__global__ void k_diag_w(const int* __restrict__ rowptr, const int* __restrict__ col, const double* __restrict__ val,
+                         int n, double* dw)
+{
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= n) return;
+    double s = 0.0;
+    for (int k = rowptr[I]; k < rowptr[I + 1]; ++k)
+        if (col[k] == I) {
+            const double* v = val + static_cast<int64_t>(k) * B * B;
+#pragma unroll
+            for (int e = 0; e < B * B; ++e) s = __dadd_rn(s, __dmul_rn(v[e], v[e]));
+        }
+    dw[I] = s;
+}
+
+// flag: 0 weak, 1 strong, 2 too close to call on the device
+template <int B>
+__global__ void k_strength(const int* __restrict__ rowptr, const int* __restrict__ col, const double* __restrict__ val,
+                           int n, const double* __restrict__ dw, double theta, unsigned char* flag, double* s2out,
+                           int* n_amb)
+{
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= n) return;
+    const double dI = dw[I];
+    for (int k = rowptr[I]; k < rowptr[I + 1]; ++k) {
+        const int J = col[k];
+        unsigned char f = 0;
+        if (J != I) {
+            const double* v = val + static_cast<int64_t>(k) * B * B;
+            double s2 = 0.0;
+#pragma unroll
+            for (int e = 0; e < B * B; ++e) s2 = __dadd_rn(s2, __dmul_rn(v[e], v[e]));
+            s2out[k] = s2;
+            const double dJ = dw[J];
+            if (dI > 0.0 && dJ > 0.0) {
+                const double lhs = sqrt(s2);
+                const double rhs = theta * pow(__dmul_rn(dI, dJ), 0.25);
+                if (fabs(lhs - rhs) <= 1e-12 * rhs) {
+                    f = 2;
+                    atomicAdd(n_amb, 1);
+                } else {
+                    f = lhs > rhs ? 1 : 0;
+                }
+            }
+        }
+        flag[k] = f;
+    }
+}
+
+__global__ void k_symmetrize(const int* __restrict__ rowptr, const int* __restrict__ col,
+                             const unsigned char* __restrict__ flag, int n, unsigned char* sym, int* cnt)
+{
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= n) return;
+    int c = 0;
+    for (int k = rowptr[I]; k < rowptr[I + 1]; ++k) {
+        const int J = col[k];
+        unsigned char s = 0;
+        if (J != I) {
+            s = flag[k] == 1;
+            if (!s) {
+                int lo = rowptr[J], hi = rowptr[J + 1];
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (col[mid] < I) lo = mid + 1;
+                    else hi = mid;
+                }
+                if (lo < rowptr[J + 1] && col[lo] == I) s = flag[lo] == 1;
+            }
+        }
+        sym[k] = s;
+        c += s;
+    }
+    cnt[I] = c;
+}
+
+// ---- elementwise helpers --------------------------------------------------
+template <int B>
+__global__ void k_invdiag(const int* __restrict__ rowptr, const int* __restrict__ col, const double* __restrict__ val,
+                          int n, double* invd)
+{
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= n) return;
+    double d[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) d[r] = 0.0;
+    for (int k = rowptr[I]; k < rowptr[I + 1]; ++k)
+        if (col[k] == I) {
+#pragma unroll
+            for (int r = 0; r < B; ++r) d[r] = val[static_cast<int64_t>(k) * B * B + r * B + r];
+        }
+#pragma unroll
+    for (int r = 0; r < B; ++r) invd[static_cast<int64_t>(I) * B + r] = d[r] != 0.0 ? 1.0 / d[r] : 1.0;
+}
+
+// row-sequential y = A x (csr.cpp:11-18 order, no FMA)
+template <int RB, int CB>
+__global__ void k_spmv_seq(const int* __restrict__ rowptr, const int* __restrict__ col, const double* __restrict__ val,
+                           int n, const double* __restrict__ x, double* y)
+{
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= n) return;
+    double acc[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) acc[r] = 0.0;
+    for (int k = rowptr[I]; k < rowptr[I + 1]; ++k) {
+        const int c = col[k];
+        const double* v = val + static_cast<int64_t>(k) * RB * CB;
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int d = 0; d < CB; ++d)
+                acc[r] = __dadd_rn(acc[r], __dmul_rn(v[r * CB + d], x[static_cast<int64_t>(c) * CB + d]));
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r) y[static_cast<int64_t>(I) * RB + r] = acc[r];
+}
+
+__global__ void k_mul_vec(double* w, const double* __restrict__ s, int64_t n)
+{
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) w[i] = __dmul_rn(w[i], s[i]);
+}
+
+__global__ void k_scale_into(double* v, const double* __restrict__ w, double s, int64_t n)
+{
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = __dmul_rn(w[i], s);
+}
+
+// csr_scale_rows (csr.cpp:200-205): val *= s[row]
+template <int RB, int CB>
+__global__ void k_scale_rows(const int* __restrict__ rowptr, double* val, int n, const double* __restrict__ s)
+{
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= n) return;
+    for (int k = rowptr[I]; k < rowptr[I + 1]; ++k)
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int d = 0; d < CB; ++d)
+                val[static_cast<int64_t>(k) * RB * CB + r * CB + d] =
+                    __dmul_rn(val[static_cast<int64_t>(k) * RB * CB + r * CB + d], s[static_cast<int64_t>(I) * RB + r]);
+}
+
+// ---- SpGEMM (csr_matmul, csr.cpp:132-166) ----------------------------------
+__global__ void k_cand_count(const int* __restrict__ arp, const int* __restrict__ acol, const int* __restrict__ brp,
+                             int n, int64_t* cnt)
+{
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= n) return;
+    int64_t c = 0;
+    for (int k = arp[I]; k < arp[I + 1]; ++k) c += brp[acol[k] + 1] - brp[acol[k]];
+    cnt[I] = c;
+}
+
+__global__ void k_cand_fill(const int* __restrict__ arp, const int* __restrict__ acol, const int* __restrict__ brp,
+                            const int* __restrict__ bcol, int r0, int r1, const int* __restrict__ seg, int* keys)
+{
+    const int I = r0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= r1) return;
+    int o = seg[I - r0];
+    for (int k = arp[I]; k < arp[I + 1]; ++k) {
+        const int K = acol[k];
+        for (int kb = brp[K]; kb < brp[K + 1]; ++kb) keys[o++] = bcol[kb];
+    }
+}
+
+__global__ void k_unique_count(const int* __restrict__ keys, const int* __restrict__ seg, int nseg, int* ucnt)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nseg) return;
+    int c = 0;
+    for (int k = seg[i]; k < seg[i + 1]; ++k) c += (k == seg[i] || keys[k] != keys[k - 1]);
+    ucnt[i] = c;
+}
+
+__global__ void k_unique_write(const int* __restrict__ keys, const int* __restrict__ seg, int nseg,
+                               const int* __restrict__ uoff, int* out)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nseg) return;
+    int o = uoff[i];
+    for (int k = seg[i]; k < seg[i + 1]; ++k)
+        if (k == seg[i] || keys[k] != keys[k - 1]) out[o++] = keys[k];
+}
+
+// One thread per scalar row (I, c) of C: every product a*b is added to its
+// C entry in (A column, B column) traversal order, mul and add rounded
+// separately -- the order and rounding of csr_matmul.
+template <int RA, int KA, int CB>
+__global__ void k_spgemm_numeric(const int* __restrict__ arp, const int* __restrict__ acol,
+                                 const double* __restrict__ aval, const int* __restrict__ brp,
+                                 const int* __restrict__ bcol, const double* __restrict__ bval,
+                                 const int* __restrict__ crp, const int* __restrict__ ccol, double* cval, int n)
+{
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int I = static_cast<int>(t / RA), c = static_cast<int>(t % RA);
+    if (I >= n) return;
+    const int c0 = crp[I], c1 = crp[I + 1];
+    for (int k = arp[I]; k < arp[I + 1]; ++k) {
+        const int K = acol[k];
+        const int b0 = brp[K], b1 = brp[K + 1];
+        if (b0 == b1) continue;
+        // position of B row K's first column in C row I, then advance monotonically
+        int lo = c0, hi = c1;
+        const int j0 = bcol[b0];
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (ccol[mid] < j0) lo = mid + 1;
+            else hi = mid;
+        }
+#pragma unroll
+        for (int d = 0; d < KA; ++d) {
+            const double a = aval[static_cast<int64_t>(k) * RA * KA + c * KA + d];
+            int pos = lo;
+            for (int kb = b0; kb < b1; ++kb) {
+                const int J = bcol[kb];
+                while (ccol[pos] < J) ++pos;
+                const double* bv = bval + static_cast<int64_t>(kb) * KA * CB + d * CB;
+                double* cv = cval + static_cast<int64_t>(pos) * RA * CB + c * CB;
+#pragma unroll
+                for (int e = 0; e < CB; ++e) cv[e] = __dadd_rn(cv[e], __dmul_rn(a, bv[e]));
+            }
+        }
+    }
+}
+
+// ---- csr_add (csr.cpp:168-198) on block rows -------------------------------
+__global__ void k_add_count(const int* __restrict__ arp, const int* __restrict__ acol, const int* __restrict__ brp,
+                            const int* __restrict__ bcol, int n, int* cnt)
+{
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= n) return;
+    int ka = arp[I], kb = brp[I], c = 0;
+    const int ea = arp[I + 1], eb = brp[I + 1];
+    while (ka < ea || kb < eb) {
+        if (kb >= eb || (ka < ea && acol[ka] < bcol[kb])) ++ka;
+        else if (ka >= ea || bcol[kb] < acol[ka]) ++kb;
+        else {
+            ++ka;
+            ++kb;
+        }
+        ++c;
+    }
+    cnt[I] = c;
+}
+
+template <int E>
+__global__ void k_add_fill(const int* __restrict__ arp, const int* __restrict__ acol, const double* __restrict__ aval,
+                           const int* __restrict__ brp, const int* __restrict__ bcol, const double* __restrict__ bval,
+                           int n, double alpha, double beta, const int* __restrict__ crp, int* ccol, double* cval)
+{
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= n) return;
+    int ka = arp[I], kb = brp[I], o = crp[I];
+    const int ea = arp[I + 1], eb = brp[I + 1];
+    while (ka < ea || kb < eb) {
+        double* cv = cval + static_cast<int64_t>(o) * E;
+        if (kb >= eb || (ka < ea && acol[ka] < bcol[kb])) {
+            ccol[o] = acol[ka];
+#pragma unroll
+            for (int e = 0; e < E; ++e) cv[e] = __dmul_rn(alpha, aval[static_cast<int64_t>(ka) * E + e]);
+            ++ka;
+        } else if (ka >= ea || bcol[kb] < acol[ka]) {
+            ccol[o] = bcol[kb];
+#pragma unroll
+            for (int e = 0; e < E; ++e) cv[e] = __dmul_rn(beta, bval[static_cast<int64_t>(kb) * E + e]);
+            ++kb;
+        } else {
+            ccol[o] = acol[ka];
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+                cv[e] = __dadd_rn(__dmul_rn(alpha, aval[static_cast<int64_t>(ka) * E + e]),
+                                  __dmul_rn(beta, bval[static_cast<int64_t>(kb) * E + e]));
+            ++ka;
+            ++kb;
+        }
+        ++o;
+    }
+}
+
+// ---- transpose (csr.cpp:39-57) ---------------------------------------------
+__global__ void k_row_of_block(const int* __restrict__ rowptr, int n, int* row)
+{
+    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= n) return;
+    for (int k = rowptr[I]; k < rowptr[I + 1]; ++k) row[k] = I;
+}
+
+__global__ void k_col_hist(const int* __restrict__ col, int64_t nnz, int* cnt)
+{
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k < nnz) atomicAdd(cnt + col[k], 1);
+}
+
+template <int RB, int CB>
+__global__ void k_transpose_fill(const int* __restrict__ perm, const int* __restrict__ row_of,
+                                 const double* __restrict__ val, int64_t nnz, int* tcol, double* tval)
+{
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= nnz) return;
+    const int src = perm[k];
+    tcol[k] = row_of[src];
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+#pragma unroll
+        for (int c = 0; c < CB; ++c)
+            tval[k * RB * CB + c * RB + r] = val[static_cast<int64_t>(src) * RB * CB + r * CB + c];
+}
+
+// gather natural rows into level order: stored row s <- natural row perm[s]
+__global__ void k_gather_rows(const int* __restrict__ rp_nat, const double* __restrict__ val_nat,
+                              const int* __restrict__ perm, int n, int E, const int* __restrict__ rp_out, double* val_out)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const int I = perm ? perm[s] : s;
+    const int k0 = rp_nat[I], len = rp_nat[I + 1] - k0, o = rp_out[s];
+    for (int k = 0; k < len; ++k)
+        for (int e = 0; e < E; ++e) val_out[static_cast<int64_t>(o + k) * E + e] = val_nat[static_cast<int64_t>(k0 + k) * E + e];
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+
+void exclusive_scan_host(const std::vector<int>& cnt, std::vector<int>& off)
+{
+    off.assign(cnt.size() + 1, 0);
+    int64_t acc = 0;
+    for (size_t i = 0; i < cnt.size(); ++i) {
+        acc += cnt[i];
+        if (acc >= (1LL << 31)) throw Error(ED_UNSUPPORTED, "block count exceeds int32");
+        off[i + 1] = static_cast<int>(acc);
+    }
+}
+
+DBsr natural_copy(const Bsr& A, cudaStream_t s)
+{
+    const BsrStruct& S = *A.st;
+    DBsr N;
+    N.nbr = S.nbr;
+    N.nbc = S.nbc;
+    N.Rb = S.Rb;
+    N.Cb = S.Cb;
+    N.nnzb = S.nnzb;
+    const int n = S.nbr, E = S.Rb * S.Cb;
+    DevArray<int> len(n);
+    k_rowlen_nat<<<g1(n), kT, 0, s>>>(S.rowptr.p, S.inv.p, n, len.p);
+    after_launch("k_rowlen_nat");
+    std::vector<int> off;
+    exclusive_scan_host(len.to_host(s), off);
+    N.rowptr.upload(off, s);
+    N.col.alloc(N.nnzb);
+    N.val.alloc(N.nnzb * E);
+    k_copy_rows<<<g1(n), kT, 0, s>>>(S.rowptr.p, S.col.p, A.val.p, S.inv.p, n, E, N.rowptr.p, N.col.p, N.val.p);
+    after_launch("k_copy_rows");
+    ED_CUDA(cudaStreamSynchronize(s));
+    return N;
+}
+
+// symbolic + numeric C = A B
+DBsr spgemm(const DBsr& A, const DBsr& B, cudaStream_t s)
+{
+    if (A.Cb != B.Rb || A.nbc != B.nbr) throw Error(ED_INVALID_ARGUMENT, "spgemm: shape mismatch");
+    DBsr C;
+    C.nbr = A.nbr;
+    C.nbc = B.nbc;
+    C.Rb = A.Rb;
+    C.Cb = B.Cb;
+    const int n = A.nbr;
+    DevArray<int64_t> cnt(n);
+    k_cand_count<<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, B.rowptr.p, n, cnt.p);
+    after_launch("k_cand_count");
+    const std::vector<int64_t> hc = cnt.to_host(s);
+    cnt.release();
+    std::vector<int> ucnt_all(n, 0);
+    std::vector<DevArray<int>> chunk_cols;
+    std::vector<int64_t> chunk_tot;
+    const int64_t kChunk = 1LL << 28; // candidates per chunk (1 GiB of int keys)
+    int r0 = 0;
+    while (r0 < n) {
+        int r1 = r0;
+        int64_t tot = 0;
+        while (r1 < n && (r1 == r0 || tot + hc[r1] <= kChunk)) tot += hc[r1++];
+        if (tot >= (1LL << 31)) throw Error(ED_UNSUPPORTED, "spgemm: row candidates exceed int32");
+        const int nseg = r1 - r0;
+        std::vector<int> seg(nseg + 1, 0);
+        for (int i = 0; i < nseg; ++i) seg[i + 1] = seg[i] + static_cast<int>(hc[r0 + i]);
+        DevArray<int> dseg;
+        dseg.upload(seg, s);
+        DevArray<int> keys(std::max<int64_t>(tot, 1)), sorted(std::max<int64_t>(tot, 1));
+        k_cand_fill<<<g1(nseg), kT, 0, s>>>(A.rowptr.p, A.col.p, B.rowptr.p, B.col.p, r0, r1, dseg.p, keys.p);
+        after_launch("k_cand_fill");
+        size_t tb = 0;
+        cub::DeviceSegmentedSort::SortKeys(nullptr, tb, keys.p, sorted.p, static_cast<int>(tot), nseg, dseg.p,
+                                           dseg.p + 1, s);
+        DevArray<unsigned char> tmp(std::max<size_t>(tb, 1));
+        ED_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp.p, tb, keys.p, sorted.p, static_cast<int>(tot), nseg, dseg.p,
+                                                   dseg.p + 1, s));
+        after_launch("cub_segmented_sort");
+        keys.release();
+        DevArray<int> uc(nseg);
+        k_unique_count<<<g1(nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, uc.p);
+        after_launch("k_unique_count");
+        const std::vector<int> huc = uc.to_host(s);
+        std::vector<int> uoff;
+        exclusive_scan_host(huc, uoff);
+        DevArray<int> duoff;
+        duoff.upload(uoff, s);
+        DevArray<int> cols(std::max(uoff[nseg], 1));
+        k_unique_write<<<g1(nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, duoff.p, cols.p);
+        after_launch("k_unique_write");
+        for (int i = 0; i < nseg; ++i) ucnt_all[r0 + i] = huc[i];
+        chunk_tot.push_back(uoff[nseg]);
+        chunk_cols.push_back(std::move(cols));
+        ED_CUDA(cudaStreamSynchronize(s));
+        r0 = r1;
+    }
+    std::vector<int> rp;
+    exclusive_scan_host(ucnt_all, rp);
+    C.nnzb = rp[n];
+    C.rowptr.upload(rp, s);
+    C.col.alloc(std::max<int64_t>(C.nnzb, 1));
+    int64_t o = 0;
+    for (size_t i = 0; i < chunk_cols.size(); ++i) {
+        if (chunk_tot[i])
+            ED_CUDA(cudaMemcpyAsync(C.col.p + o, chunk_cols[i].p, chunk_tot[i] * sizeof(int), cudaMemcpyDeviceToDevice, s));
+        o += chunk_tot[i];
+    }
+    const int E = C.Rb * C.Cb;
+    C.val.alloc(std::max<int64_t>(C.nnzb * E, 1));
+    C.val.zero(s);
+    const int64_t threads = static_cast<int64_t>(n) * A.Rb;
+    if (A.Rb == 3 && A.Cb == 3 && B.Cb == 3)
+        k_spgemm_numeric<3, 3, 3><<<g1(threads), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, B.rowptr.p, B.col.p,
+                                                             B.val.p, C.rowptr.p, C.col.p, C.val.p, n);
+    else if (A.Rb == 1 && A.Cb == 1 && B.Cb == 1)
+        k_spgemm_numeric<1, 1, 1><<<g1(threads), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, B.rowptr.p, B.col.p,
+                                                             B.val.p, C.rowptr.p, C.col.p, C.val.p, n);
+    else
+        throw Error(ED_UNSUPPORTED, "spgemm: unsupported block shape");
+    after_launch("k_spgemm_numeric");
+    ED_CUDA(cudaStreamSynchronize(s));
+    return C;
+}
+
+DBsr add(const DBsr& A, const DBsr& B, double alpha, double beta, cudaStream_t s)
+{
+    DBsr C;
+    C.nbr = A.nbr;
+    C.nbc = A.nbc;
+    C.Rb = A.Rb;
+    C.Cb = A.Cb;
+    const int n = A.nbr;
+    DevArray<int> cnt(n);
+    k_add_count<<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, B.rowptr.p, B.col.p, n, cnt.p);
+    after_launch("k_add_count");
+    std::vector<int> rp;
+    exclusive_scan_host(cnt.to_host(s), rp);
+    C.nnzb = rp[n];
+    C.rowptr.upload(rp, s);
+    C.col.alloc(std::max<int64_t>(C.nnzb, 1));
+    const int E = C.Rb * C.Cb;
+    C.val.alloc(std::max<int64_t>(C.nnzb * E, 1));
+    if (E == 9)
+        k_add_fill<9><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, B.rowptr.p, B.col.p, B.val.p, n, alpha, beta,
+                                           C.rowptr.p, C.col.p, C.val.p);
+    else
+        k_add_fill<1><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, B.rowptr.p, B.col.p, B.val.p, n, alpha, beta,
+                                           C.rowptr.p, C.col.p, C.val.p);
+    after_launch("k_add_fill");
+    ED_CUDA(cudaStreamSynchronize(s));
+    return C;
+}
+
+DBsr transpose(const DBsr& P, cudaStream_t s)
+{
+    DBsr R;
+    R.nbr = P.nbc;
+    R.nbc = P.nbr;
+    R.Rb = P.Cb;
+    R.Cb = P.Rb;
+    R.nnzb = P.nnzb;
+    const int64_t nnz = P.nnzb;
+    DevArray<int> row_of(std::max<int64_t>(nnz, 1)), idx(std::max<int64_t>(nnz, 1)), keys_out(std::max<int64_t>(nnz, 1)),
+        perm(std::max<int64_t>(nnz, 1));
+    k_row_of_block<<<g1(P.nbr), kT, 0, s>>>(P.rowptr.p, P.nbr, row_of.p);
+    after_launch("k_row_of_block");
+    std::vector<int> iota(nnz);
+    std::iota(iota.begin(), iota.end(), 0);
+    idx.upload(iota, s);
+    int bits = 1;
+    while ((1LL << bits) < R.nbr + 1) ++bits;
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, P.col.p, keys_out.p, idx.p, perm.p, static_cast<int>(nnz), 0, bits, s);
+    DevArray<unsigned char> tmp(std::max<size_t>(tb, 1));
+    ED_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, P.col.p, keys_out.p, idx.p, perm.p, static_cast<int>(nnz), 0, bits,
+                                            s)); // stable: equal columns keep ascending source rows
+    after_launch("cub_radix_sort");
+    DevArray<int> cnt(R.nbr);
+    cnt.zero(s);
+    k_col_hist<<<g1(nnz), kT, 0, s>>>(P.col.p, nnz, cnt.p);
+    after_launch("k_col_hist");
+    std::vector<int> rp;
+    exclusive_scan_host(cnt.to_host(s), rp);
+    R.rowptr.upload(rp, s);
+    R.col.alloc(std::max<int64_t>(nnz, 1));
+    R.val.alloc(std::max<int64_t>(nnz * P.Rb * P.Cb, 1));
+    if (P.Rb == 3 && P.Cb == 3)
+        k_transpose_fill<3, 3><<<g1(nnz), kT, 0, s>>>(perm.p, row_of.p, P.val.p, nnz, R.col.p, R.val.p);
+    else
+        k_transpose_fill<1, 1><<<g1(nnz), kT, 0, s>>>(perm.p, row_of.p, P.val.p, nnz, R.col.p, R.val.p);
+    after_launch("k_transpose_fill");
+    ED_CUDA(cudaStreamSynchronize(s));
+    return R;
+}
+
+HostCsr to_host_csr(const DBsr& M, cudaStream_t s)
+{
+    Bsr tmp;
+    auto st = std::make_shared<BsrStruct>();
+    st->Rb = M.Rb;
+    st->Cb = M.Cb;
+    st->nbr = M.nbr;
+    st->nbc = M.nbc;
+    st->nnzb = M.nnzb;
+    st->h_rowptr = M.rowptr.to_host(s);
+    std::vector<int> c = M.col.to_host(s);
+    c.resize(M.nnzb);
+    st->h_col = c;
+    tmp.st = st;
+    tmp.val.copy_from(M.val, s);
+    return bsr_to_csr(tmp, s);
+}
+
+DBsr upload_block(const HostCsr& a, int Rb, int Cb, cudaStream_t s)
+{
+    const BlockPattern pat = block_pattern_of_csr(a, Rb, Cb);
+    const std::vector<double> v = block_values_of_csr(a, pat, Rb, Cb);
+    DBsr M;
+    M.nbr = pat.nbr;
+    M.nbc = pat.nbc;
+    M.Rb = Rb;
+    M.Cb = Cb;
+    M.nnzb = pat.nnzb();
+    std::vector<int> rp(pat.rowptr.begin(), pat.rowptr.end());
+    M.rowptr.upload(rp, s);
+    M.col.upload(pat.col, s);
+    M.val.upload(v, s);
+    ED_CUDA(cudaStreamSynchronize(s));
+    return M;
+}
+
+} // namespace
+
+Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s)
+{
+    Bsr out;
+    if (!leveled) {
+        auto st = std::make_shared<BsrStruct>();
+        st->Rb = m.Rb;
+        st->Cb = m.Cb;
+        st->nbr = m.nbr;
+        st->nbc = m.nbc;
+        st->nnzb = m.nnzb;
+        int L = 2;
+        const double avg = m.nbr ? static_cast<double>(m.nnzb) / m.nbr : 1.0;
+        while (L < 32 && L * 2 < avg) L *= 2;
+        st->L = L;
+        st->rowptr = std::move(m.rowptr);
+        st->col = std::move(m.col);
+        st->lev_ptr = {0, m.nbr};
+        out.st = st;
+        out.val = std::move(m.val);
+        return out;
+    }
+    // level schedule needs the pattern on the host
+    BlockPattern pat;
+    pat.nbr = m.nbr;
+    pat.nbc = m.nbc;
+    const std::vector<int> rp = m.rowptr.to_host(s);
+    pat.rowptr.assign(rp.begin(), rp.end());
+    pat.col = m.col.to_host(s);
+    pat.col.resize(m.nnzb);
+    if (!pattern_symmetric(pat)) throw Error(ED_UNSUPPORTED, "Gauss-Seidel operator pattern is not symmetric");
+    std::vector<int> order, lvl;
+    int nlev = 0;
+    gs_level_order(pat, order, lvl, nlev);
+    const BsrLayout lay = make_layout(pat, order, lvl);
+    out.st = bsr_make_struct(pat, lay, m.Rb, m.Cb, s);
+    out.st->leveled = true;
+    const int E = m.Rb * m.Cb;
+    out.val.alloc(std::max<int64_t>(m.nnzb * E, 1));
+    k_gather_rows<<<g1(m.nbr), kT, 0, s>>>(m.rowptr.p, m.val.p, out.st->perm.p ? out.st->perm.p : nullptr, m.nbr, E,
+                                           out.st->rowptr.p, out.val.p);
+    after_launch("k_gather_rows");
+    ED_CUDA(cudaStreamSynchronize(s));
+    return out;
+}
+
+DevSetupResult amg_build_device(const Bsr& A0, const AmgOpts& opts, cudaStream_t s)
+{
+    const int k = opts.block_size;
+    const int Bs = A0.st->Rb;
+    if (k != Bs || (Bs != 1 && Bs != 3)) throw Error(ED_UNSUPPORTED, "device AMG setup needs block size == storage block");
+    Timer T;
+    DevSetupResult res;
+    DBsr A = natural_copy(A0, s);
+    const int nrows0 = A.nbr * Bs;
+    // Row grouping: explicit maps (set_amg_maps) must describe consecutive runs of k
+    if (!opts.row_to_node.empty()) {
+        for (int r = 0; r < nrows0; ++r)
+            if (opts.row_to_node[r] != r / k || opts.row_component[r] != r % k)
+                throw Error(ED_UNSUPPORTED, "device AMG setup needs consecutive node rows");
+    }
+    std::vector<double> Bn(static_cast<size_t>(nrows0) * k, 0.0);
+    for (int r = 0; r < nrows0; ++r) Bn[static_cast<size_t>(r) * k + r % k] = 1.0;
+    T.lap(s, "start", 0, A.nbr, A.nnzb);
+
+    while (A.nbr * Bs > opts.coarse_max_rows && static_cast<int>(res.levels.size()) + 1 < opts.max_levels) {
+        const int lvl = static_cast<int>(res.levels.size());
+        const int n = A.nbr;
+        // strength graph
+        DevArray<double> dw(n), s2(std::max<int64_t>(A.nnzb, 1));
+        DevArray<unsigned char> flag(std::max<int64_t>(A.nnzb, 1)), sym(std::max<int64_t>(A.nnzb, 1));
+        DevArray<int> namb(1), scnt(n);
+        namb.zero(s);
+        if (Bs == 3) {
+            k_diag_w<3><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, dw.p);
+            k_strength<3><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, dw.p, opts.strength_theta, flag.p,
+                                               s2.p, namb.p);
+        } else {
+            k_diag_w<1><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, dw.p);
+            k_strength<1><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, dw.p, opts.strength_theta, flag.p,
+                                               s2.p, namb.p);
+        }
+        after_launch("k_strength");
+        const int amb = namb.to_host(s)[0];
+        if (amb > 0) {
+            // re-decide borderline comparisons with the host's libm pow (amg.cpp:65)
+            std::vector<unsigned char> hf = flag.to_host(s);
+            const std::vector<double> hs2 = s2.to_host(s), hdw = dw.to_host(s);
+            const std::vector<int> hrp = A.rowptr.to_host(s), hcol = A.col.to_host(s);
+            for (int I = 0; I < n; ++I)
+                for (int kk = hrp[I]; kk < hrp[I + 1]; ++kk)
+                    if (hf[kk] == 2)
+                        hf[kk] = std::sqrt(hs2[kk]) > opts.strength_theta * std::pow(hdw[I] * hdw[hcol[kk]], 0.25);
+            flag.upload(hf, s);
+        }
+        s2.release();
+        k_symmetrize<<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, flag.p, n, sym.p, scnt.p);
+        after_launch("k_symmetrize");
+        T.lap(s, "strength", lvl, n, amb);
+        // neighbour lists -> host aggregation
+        std::vector<int64_t> nptr(n + 1, 0);
+        {
+            const std::vector<int> c = scnt.to_host(s);
+            for (int I = 0; I < n; ++I) nptr[I + 1] = nptr[I] + c[I];
+        }
+        std::vector<int> nbr(nptr[n]);
+        {
+            const std::vector<unsigned char> hs = sym.to_host(s);
+            const std::vector<int> hrp = A.rowptr.to_host(s), hcol = A.col.to_host(s);
+            for (int I = 0; I < n; ++I) {
+                int64_t o = nptr[I];
+                for (int kk = hrp[I]; kk < hrp[I + 1]; ++kk)
+                    if (hs[kk]) nbr[o++] = hcol[kk];
+            }
+        }
+        flag.release();
+        sym.release();
+        std::vector<int> agg_of_node;
+        const int n_agg = amg_aggregate(nptr, nbr, agg_of_node);
+        T.lap(s, "aggregate", lvl, n_agg, 0);
+        if (n_agg <= 0 || n_agg >= n) {
+            if (res.levels.empty()) {
+                res.fallback = true;
+                DevArray<double> inv(nrows0);
+                if (Bs == 3) k_invdiag<3><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, inv.p);
+                else k_invdiag<1><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, inv.p);
+                after_launch("k_invdiag");
+                res.fallback_inv_diag = inv.to_host(s);
+                return res;
+            }
+            break;
+        }
+        // tentative prolongator (host, tiny)
+        const int nrows = n * Bs;
+        std::vector<int> agg_of_row(nrows);
+        for (int r = 0; r < nrows; ++r) agg_of_row[r] = agg_of_node[r / Bs];
+        std::vector<double> Bc;
+        const HostCsr Pt_h = amg_tentative(nrows, k, agg_of_row, n_agg, Bn, Bc);
+        DBsr Pt = upload_block(Pt_h, Bs, k, s);
+        T.lap(s, "tentative", lvl, Pt.nbr, Pt.nnzb);
+        // inverse diagonal + spectral radius of D^-1 A (amg.cpp:170-185)
+        DevLevelData L;
+        L.invd.alloc(nrows);
+        if (Bs == 3) k_invdiag<3><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, L.invd.p);
+        else k_invdiag<1><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, L.invd.p);
+        after_launch("k_invdiag");
+        L.inv_diag = L.invd.to_host(s);
+        double omega = 0.0;
+        if (opts.smooth_prolongator) {
+            DevArray<double> v(nrows), w(nrows);
+            vec_fill(v.p, 1.0, nrows, s);
+            std::vector<double> hv(nrows, 1.0), hw(nrows);
+            double lambda = 1.0;
+            bool zero = false;
+            for (int it = 0; it < 10; ++it) {
+                if (Bs == 3) k_spmv_seq<3, 3><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, v.p, w.p);
+                else k_spmv_seq<1, 1><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, v.p, w.p);
+                k_mul_vec<<<g1(nrows), kT, 0, s>>>(w.p, L.invd.p, nrows);
+                after_launch("k_spmv_seq");
+                w.download(hw.data(), s);
+                ED_CUDA(cudaStreamSynchronize(s));
+                const double nrm = amg_seq_norm(hw);
+                if (nrm == 0.0) {
+                    lambda = 1.0;
+                    zero = true;
+                    break;
+                }
+                lambda = nrm / amg_seq_norm(hv);
+                const double inv = 1.0 / nrm;
+                for (int i = 0; i < nrows; ++i) hv[i] = hw[i] * inv;
+                k_scale_into<<<g1(nrows), kT, 0, s>>>(v.p, w.p, inv, nrows);
+                after_launch("k_scale_into");
+            }
+            (void)zero;
+            omega = 4.0 / (3.0 * std::max(lambda, 1e-12));
+            T.lap(s, "spectral", lvl, nrows, 0);
+            DBsr APt = spgemm(A, Pt, s);
+            T.lap(s, "AP_tent", lvl, APt.nbr, APt.nnzb);
+            if (Bs == 3) k_scale_rows<3, 3><<<g1(n), kT, 0, s>>>(APt.rowptr.p, APt.val.p, n, L.invd.p);
+            else k_scale_rows<1, 1><<<g1(n), kT, 0, s>>>(APt.rowptr.p, APt.val.p, n, L.invd.p);
+            after_launch("k_scale_rows");
+            L.P = add(Pt, APt, 1.0, -omega, s);
+            T.lap(s, "smooth_P", lvl, L.P.nbr, L.P.nnzb);
+        } else {
+            L.P = std::move(Pt);
+        }
+        L.R = transpose(L.P, s);
+        T.lap(s, "transpose", lvl, L.R.nbr, L.R.nnzb);
+        DBsr AP = spgemm(A, L.P, s);
+        T.lap(s, "AP", lvl, AP.nbr, AP.nnzb);
+        DBsr Ac = spgemm(L.R, AP, s);
+        T.lap(s, "RAP", lvl, Ac.nbr, Ac.nnzb);
+        L.A = std::move(A);
+        res.levels.push_back(std::move(L));
+        A = std::move(Ac);
+        Bn = std::move(Bc);
+    }
+    // coarsest level: dense COD on the host (amg.cpp:278-294)
+    DevLevelData L;
+    const int n = A.nbr;
+    const int nr = n * Bs;
+    L.invd.alloc(nr);
+    if (Bs == 3) k_invdiag<3><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, L.invd.p);
+    else k_invdiag<1><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, L.invd.p);
+    after_launch("k_invdiag");
+    L.inv_diag = L.invd.to_host(s);
+    const HostCsr Ah = to_host_csr(A, s);
+    std::vector<double> dense(static_cast<size_t>(nr) * nr, 0.0);
+    for (int r = 0; r < nr; ++r)
+        for (int64_t kk = Ah.rowptr[r]; kk < Ah.rowptr[r + 1]; ++kk)
+            dense[static_cast<size_t>(Ah.col[kk]) * nr + r] = Ah.val[kk];
+    res.pinv = cod_pinv(dense, nr, 1e-12);
+    res.nc = nr;
+    L.A = std::move(A);
+    res.levels.push_back(std::move(L));
+    T.lap(s, "coarse_cod", static_cast<int>(res.levels.size()) - 1, nr, 0);
+    return res;
+}
+
+} // namespace edb

@@ -1,0 +1,51 @@
+// Smoothed-aggregation AMG setup on the GPU (amg.cpp:189-295).
+//
+// The numeric steps run on the device with the reference's per-entry
+// arithmetic order and no FMA contraction, so the hierarchy is bitwise the
+// reference's:
+//   strength graph  -- per block s2 = sum v^2 in row-major block order
+//                      (amg.cpp:36-67); comparisons within 1e-12 of the
+//                      threshold are re-decided on the host with libm pow
+//   aggregation     -- host, sequential greedy (amg.cpp:85-117)
+//   tentative P     -- host per-aggregate MGS (amg.cpp:122-168), tiny
+//   spectral radius -- device row-sequential SpMV, host sequential norms
+//   SpGEMM          -- symbolic: CUB segmented sort of candidate columns;
+//                      numeric: one thread per scalar row accumulating in
+//                      (A column, B column) traversal order (csr.cpp:132-166)
+//   transpose       -- stable CUB radix sort by block column (csr.cpp:39-57)
+#pragma once
+
+#include "amg_host.hpp"
+#include "ed_internal.hpp"
+
+namespace edb {
+
+// Natural-order block CSR on the device.
+struct DBsr {
+    int nbr = 0, nbc = 0, Rb = 1, Cb = 1;
+    int64_t nnzb = 0;
+    DevArray<int> rowptr, col;
+    DevArray<double> val;
+};
+
+struct DevLevelData {
+    DBsr A, P, R;                 // P, R empty on the coarsest level
+    std::vector<double> inv_diag; // host copy (small enough; uploaded by the caller)
+    DevArray<double> invd;
+};
+
+struct DevSetupResult {
+    std::vector<DevLevelData> levels;
+    bool fallback = false;
+    std::vector<double> fallback_inv_diag;
+    std::vector<double> pinv;
+    int nc = 0;
+};
+
+// A0 given as a (possibly level-permuted) Bsr with block size == opts.block_size.
+DevSetupResult amg_build_device(const Bsr& A0, const AmgOpts& opts, cudaStream_t s);
+
+// Helpers shared with the V-cycle construction.
+Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s);
+
+} // namespace edb

@@ -529,6 +529,46 @@ struct Cod {
 
 } // namespace
 
+int amg_aggregate(const std::vector<int64_t>& nbr_ptr, const std::vector<int>& nbr, std::vector<int>& agg_of)
+{
+    // aggregate() of amg.cpp:85-117 on a CSR neighbour list
+    const int n = static_cast<int>(nbr_ptr.size()) - 1;
+    agg_of.assign(n, -1);
+    int n_agg = 0;
+    for (int i = 0; i < n; ++i) {
+        if (agg_of[i] >= 0 || nbr_ptr[i] == nbr_ptr[i + 1]) continue;
+        bool clean = true;
+        for (int64_t k = nbr_ptr[i]; k < nbr_ptr[i + 1]; ++k)
+            if (agg_of[nbr[k]] >= 0) {
+                clean = false;
+                break;
+            }
+        if (!clean) continue;
+        agg_of[i] = n_agg;
+        for (int64_t k = nbr_ptr[i]; k < nbr_ptr[i + 1]; ++k) agg_of[nbr[k]] = n_agg;
+        ++n_agg;
+    }
+    for (int i = 0; i < n; ++i) {
+        if (agg_of[i] >= 0) continue;
+        for (int64_t k = nbr_ptr[i]; k < nbr_ptr[i + 1]; ++k)
+            if (agg_of[nbr[k]] >= 0) {
+                agg_of[i] = agg_of[nbr[k]];
+                break;
+            }
+    }
+    for (int i = 0; i < n; ++i)
+        if (agg_of[i] < 0) agg_of[i] = n_agg++;
+    return n_agg;
+}
+
+HostCsr amg_tentative(int nrows, int k, const std::vector<int>& agg_of_row, int n_agg, const std::vector<double>& B,
+                      std::vector<double>& Bc)
+{
+    return tentative_prolongator(nrows, k, agg_of_row, n_agg, B, Bc);
+}
+
+double amg_seq_norm(const std::vector<double>& v) { return seq_norm(v); }
+
 std::vector<double> cod_pinv(const std::vector<double>& dense_colmajor, int n, double threshold)
 {
     Cod cod;

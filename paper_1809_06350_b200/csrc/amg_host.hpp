@@ -39,6 +39,15 @@ struct HostHierarchy {
 
 HostHierarchy amg_build_host(const HostCsr& A0, const AmgOpts& opts);
 
+// Pieces reused by the device setup (amg_device.cu):
+// greedy aggregation on a symmetric neighbour CSR (amg.cpp:85-117)
+int amg_aggregate(const std::vector<int64_t>& nbr_ptr, const std::vector<int>& nbr, std::vector<int>& agg_of);
+// tentative prolongator + coarse near-nullspace (amg.cpp:122-168)
+HostCsr amg_tentative(int nrows, int k, const std::vector<int>& agg_of_row, int n_agg, const std::vector<double>& B,
+                      std::vector<double>& Bc);
+// (sqrt of) the sequential sum of squares, vec_norm order (csr.cpp:213-221)
+double amg_seq_norm(const std::vector<double>& v);
+
 // CSR helpers restating csr.cpp
 HostCsr csr_matmul(const HostCsr& a, const HostCsr& b);
 HostCsr csr_transpose(const HostCsr& a);

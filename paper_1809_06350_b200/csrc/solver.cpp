@@ -9,6 +9,9 @@
 #include <chrono>
 #include <cmath>
 
+#include <cstdlib>
+
+#include "amg_device.hpp"
 #include "ctx.hpp"
 
 namespace edb {
@@ -226,6 +229,46 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o)
     lv.clear();
     fallback = false;
     const double t0 = now_ms();
+    const bool device_ok = o.block_size == A0.st->Rb && (A0.st->Rb == 1 || A0.st->Rb == 3) &&
+                           std::getenv("ED_HOST_AMG") == nullptr;
+    if (device_ok) {
+        // GPU setup (amg_device.cu); the host only aggregates and orthonormalises
+        DevSetupResult R = amg_build_device(A0, o, s);
+        setup_host_ms = 0.0;
+        if (R.fallback) {
+            fallback = true;
+            fb_invd.upload(R.fallback_inv_diag, s);
+            ED_CUDA(cudaStreamSynchronize(s));
+            return;
+        }
+        const int L = static_cast<int>(R.levels.size());
+        lv.resize(L);
+        for (int l = 0; l < L; ++l) {
+            DevLevel& d = lv[l];
+            DevLevelData& D = R.levels[l];
+            d.n = D.A.nbr * D.A.Rb;
+            if (l == 0) {
+                d.A = &A0;
+            } else {
+                d.Aown = bsr_from_dbsr(std::move(D.A), true, s);
+                d.A = &d.Aown;
+            }
+            d.invd = std::move(D.invd);
+            d.s.alloc(d.n);
+            if (l > 0) {
+                d.r.alloc(d.n);
+                d.z.alloc(d.n);
+            }
+            if (l + 1 < L) {
+                d.P = bsr_from_dbsr(std::move(D.P), false, s);
+                d.R = bsr_from_dbsr(std::move(D.R), false, s);
+            }
+        }
+        nc = R.nc;
+        pinv.upload(R.pinv, s);
+        ED_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
     const HostCsr A0h = bsr_to_csr(A0, s);
     const HostHierarchy hh = amg_build_host(A0h, o);
     setup_host_ms = now_ms() - t0;
