@@ -169,3 +169,129 @@ def test_newton_first_pass_matches_reference(oracle):
     sg, sr = ctx.get_state(), P.get_state()
     for k in ("u", "udot", "p", "pdot", "v", "vdot"):
         assert _rel(getattr(sg, k), sr[k]) < X_TOL, k
+
+
+def test_device_amg_setup_equals_host_restatement(cfg0, monkeypatch):
+    """The GPU hierarchy build (amg_device.cu) and the host restatement
+    (amg_host.cpp) produce identical hierarchies -> identical V-cycles."""
+    cp, P, st, planes = cfg0
+    ctx = api.Context(0)
+    ctx.set_block_system(*[_csr(m) for m in planes])
+    r = np.random.default_rng(5).uniform(-1, 1, cp.nv)
+    opts = cp.solver_options()
+    monkeypatch.setenv("ED_HOST_AMG", "1")
+    zh, ih = ctx.amg_vcycle(r, 0, opts)
+    monkeypatch.delenv("ED_HOST_AMG")
+    zd, idv = ctx.amg_vcycle(r, 0, opts)
+    assert ih["level_rows"] == idv["level_rows"]
+    assert np.array_equal(zh, zd)
+    zh, ih = None, None
+    monkeypatch.setenv("ED_HOST_AMG", "1")
+    sh, i1 = ctx.amg_vcycle(r[: cp.np], 1, opts)
+    monkeypatch.delenv("ED_HOST_AMG")
+    sd, i2 = ctx.amg_vcycle(r[: cp.np], 1, opts)
+    assert i1["level_rows"] == i2["level_rows"] and np.array_equal(sh, sd)
+
+
+def _random_saddle(nv, np_, seed, d_shift=1.0):
+    """random_saddle of test_precond.cpp:43-67 (numpy generator)."""
+    rng = np.random.default_rng(seed)
+    A = rng.uniform(-1, 1, (nv, nv)) + (nv + 2.0) * np.eye(nv)
+    B = rng.uniform(-1, 1, (nv, np_))
+    Cm = rng.uniform(-1, 1, (np_, nv))
+    D = rng.uniform(-1, 1, (np_, np_)) + d_shift * (np_ + 2.0) * np.eye(np_)
+    return A, B, Cm, D
+
+
+@pytest.mark.parametrize("nv,np_,seed,d_shift", [(14, 8, 9, 1.0), (12, 4, 10, 0.0), (30, 11, 3, 1.0)])
+def test_solve_block_system_random_saddle(oracle, nv, np_, seed, d_shift):
+    """SolveBlockSystemMatchesDirect / HandlesZeroPressureDiagonalBlock
+    (test_precond.cpp:228-306): GPU vs reference vs dense LU."""
+    import scipy.sparse as sp
+    A, B, Cm, D = _random_saddle(nv, np_, seed, d_shift)
+    if d_shift == 0.0:
+        D = np.zeros_like(D)
+    K = np.block([[A, B], [Cm, D]])
+    b = np.random.default_rng(seed + 100).uniform(-1, 1, nv + np_)
+    blocks = [api.Csr.from_scipy(sp.csr_matrix(M)) for M in (A, B, Cm, D)]
+    if d_shift == 0.0:
+        blocks[3] = api.Csr(np_, np_, np.zeros(np_ + 1, np.int32), np.zeros(0, np.int32), np.zeros(0))
+    opts = api.block_solver_options()
+    opts.outer = api.krylov_config(500, 500, 1e-10)
+    opts.amg_a = api.amg_options(1, 0)
+    if d_shift == 0.0:
+        for c in (opts.a, opts.s, opts.inner):
+            c.rel_tol = 1e-10
+    ctx = api.Context(0)
+    ctx.set_block_system(*blocks)
+    xg, sg, hg = ctx.solve_block_system(b, opts)
+    ref_blocks = [oracle.Csr(m.nrows, m.ncols, m.rowptr, m.col, m.val) for m in blocks]
+    xr, sr, hr = oracle.solve_block_csr(*ref_blocks, b, opts_to_ref(opts))
+    x_lu = np.linalg.solve(K, b)
+    assert sg["converged"] and sr["converged"]
+    assert np.max(np.abs(xg - x_lu)) <= 1e-5 * np.linalg.norm(x_lu)
+    _assert_stats(sg, sr)
+    _assert_history(hg, hr)
+    assert _rel(xg, xr) < X_TOL
+
+
+def test_cfg1_newton_first_pass_matches_reference(oracle):
+    """BASELINE configs[1]: 40^3 cube, fully incompressible, seeded state."""
+    cp = CubeProblem.config(1)
+    P = _ref_problem(oracle, cp)
+    st = cp.seeded_state()
+    P.set_state(st.u, st.udot, st.p, st.pdot, st.v, st.vdot)
+    ctx = cp.context(0)
+    ctx.set_state(st)
+    opts = cp.solver_options()
+    out = ctx.newton_first_pass(cp.ts, opts)
+    ro = P.newton_first_pass(opts_to_ref(opts))
+    print("gpu", out["stats"], out["history"], out["times"])
+    print("ref", ro["stats"], ro["history"], ro["times"])
+    assert abs(out["norm"] - ro["norm"]) <= 1e-12 * ro["norm"]
+    _assert_stats(out["stats"], ro["stats"])
+    _assert_history(out["history"], ro["history"])
+    assert _rel(out["x"], ro["x"]) < X_TOL
+
+
+def test_fiber_material_assembly_matches_reference(oracle):
+    """DispersedFiberIsochoric (HGO-type fibres, materials.cpp:8-53) on the
+    device: residuals and all four planes vs the reference, strained state."""
+    n = 4
+    p = oracle.cube_params(n, nu=0.5)
+    p.material, p.mu, p.k1, p.k2, p.kd, p.phi_deg, p.rho0, p.incompressible = 1, 2.0, 1.5, 0.8, 0.1, 40.0, 1.0, 1
+    P = oracle.RefProblem(p)
+    cp = CubeProblem(n=n, nu=0.5)
+    st = cp.seeded_state()
+    st.u *= 20.0
+    P.set_state(st.u, st.udot, st.p, st.pdot, st.v, st.vdot)
+    m = P.mesh()
+    ctx = api.Context(0)
+    ctx.set_mesh(cp.mesh, m["tau"])
+    ctx.build_dofs(cp.fixed)
+    ctx.set_material(api.dispersed_fiber(2.0, 1.5, 0.8, 0.1, 40.0, 1.0))
+    ctx.set_loads((0.0, 0.0, 0.0), cp.load_facets, cp.load_third, cp.traction_h())
+    ctx.set_state(st)
+    rm, rp = ctx.assemble_residuals()
+    rmr, rpr, _ = P.assemble_residuals()
+    assert np.max(np.abs(rm - rmr)) <= 1e-12 * np.max(np.abs(rmr))
+    assert np.max(np.abs(rp - rpr)) <= 1e-12 * np.max(np.abs(rpr))
+    ctx.assemble_tangent(cp.ts)
+    P.assemble_tangent()
+    for k in range(4):
+        g, r = ctx.tangent_plane(k), P.tangent_plane(k)
+        assert np.array_equal(g.col, r.col)
+        assert np.max(np.abs(g.val - r.val)) <= 1e-12 * np.max(np.abs(r.val)), k
+
+
+def test_element_inversion_raises(oracle):
+    """ThrowsOnElementInversion (test_assembly.cpp:271-286): collapse x=1 onto x=0."""
+    cp = CubeProblem(n=2, nu=0.4)
+    ctx = cp.context(0)
+    st = api.State.zeros(cp.mesh.n_nodes)
+    st.u.reshape(-1, 3)[cp.mesh.nodes[:, 0] > 0.5, 0] = -2.0
+    ctx.set_state(st)
+    with pytest.raises(api.ElementInversion, match="inverted"):
+        ctx.assemble_residuals()
+    with pytest.raises(api.ElementInversion):
+        ctx.assemble_tangent(cp.ts)

@@ -215,3 +215,42 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         api.Context(0)
+
+
+def _fiber_params(n):
+    """make_fiber_material (materials.cpp:67-80) with the reference test's
+    fibre_test_material constants (test_assembly.cpp:34-37)."""
+    p = ref.cube_params(n, nu=0.5)
+    p.material, p.mu, p.k1, p.k2, p.kd, p.phi_deg, p.rho0 = 1, 2.0, 1.5, 0.8, 0.1, 40.0, 1.0
+    p.incompressible = 1
+    return p
+
+
+def _fiber_restate_mat(p):
+    phi = p.phi_deg * np.arccos(-1.0) / 180.0
+    H = []
+    for a in (np.array([np.cos(phi), np.sin(phi), 0.0]), np.array([np.cos(phi), -np.sin(phi), 0.0])):
+        H.append(np.eye(3) * p.kd + (1.0 - 3.0 * p.kd) * np.outer(a, a))
+    return dict(incompressible=True, rho0=p.rho0, mu=p.mu, kappa=0.0, k1=p.k1, k2=p.k2, H=H)
+
+
+def test_restated_fiber_material_assembly_matches_reference():
+    """DispersedFiberIsochoric stress and stress_dir (materials.cpp:21-53)
+    through residual and tangent assembly, seeded state, 3^3 cube."""
+    p = _fiber_params(3)
+    P = ref.RefProblem(p)
+    cp = CubeProblem(n=3, nu=0.5)
+    st = cp.seeded_state()
+    st.u *= 20.0  # engage the exponential fibre stiffening
+    P.set_state(st.u, st.udot, st.p, st.pdot, st.v, st.vdot)
+    mesh, dofs, _, tau, loads, sd, ts = _restate_problem(cp, P, st)
+    mat = _fiber_restate_mat(p)
+    rm, rp = R.assemble_residuals(mesh, dofs, mat, tau, loads, sd)
+    rmr, rpr, _ = P.assemble_residuals()
+    assert np.max(np.abs(rm - rmr)) <= 1e-12 * np.max(np.abs(rmr))
+    assert np.max(np.abs(rp - rpr)) <= 1e-12 * np.max(np.abs(rpr))
+    planes = R.assemble_tangent(mesh, dofs, mat, tau, loads, sd, ts)
+    P.assemble_tangent()
+    for k in range(6):
+        Mr = P.tangent_plane(k).to_scipy()
+        assert abs(planes[k] - Mr).max() <= 1e-12 * abs(Mr).max(), k
