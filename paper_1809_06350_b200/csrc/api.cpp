@@ -45,7 +45,7 @@ void after_launch(const char* what)
     if (g_prof.on) {
         cudaDeviceSynchronize();
         const auto now = std::chrono::steady_clock::now();
-        auto& slot = g_prof.t[what];
+        auto& slot = g_prof.t[prof_tag().empty() ? std::string(what) : std::string(what) + "@" + prof_tag()];
         slot.first += 1;
         slot.second += std::chrono::duration<double>(now - g_prof.last).count();
         g_prof.last = now;
@@ -53,6 +53,12 @@ void after_launch(const char* what)
 }
 
 int64_t launch_count() { return g_launches.load(); }
+
+std::string& prof_tag()
+{
+    static std::string t;
+    return t;
+}
 
 Ctx::Ctx(int dev) : device(dev)
 {

@@ -39,6 +39,7 @@ struct Error : std::runtime_error {
 // Launch bookkeeping: every kernel launcher calls this after <<<>>>.
 void after_launch(const char* what);
 int64_t launch_count();
+std::string& prof_tag(); // ED_PROFILE attribution tag (e.g. hierarchy/level)
 
 // Owning device array (move-only).
 template <class T>

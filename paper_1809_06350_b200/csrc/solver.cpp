@@ -330,8 +330,11 @@ void DevHierarchy::cycle(Ctx& c, int l, const double* r, double* z)
 {
     DevLevel& d = lv[l];
     cudaStream_t s = c.stream;
+    const std::string saved = prof_tag();
+    prof_tag() = (opts.block_size == 3 ? "A" : "S") + std::to_string(l);
     if (l == n_levels() - 1) {
         dense_gemv(pinv.p, r, z, nc, s); // COD min-norm solve (amg.cpp:331-334)
+        prof_tag() = saved;
         return;
     }
     vec_fill(z, 0.0, d.n, s);
@@ -340,8 +343,10 @@ void DevHierarchy::cycle(Ctx& c, int l, const double* r, double* z)
     DevLevel& e = lv[l + 1];
     spmv(d.R, d.s.p, e.r.p, nullptr, 0, s);
     cycle(c, l + 1, e.r.p, e.z.p);
+    prof_tag() = (opts.block_size == 3 ? "A" : "S") + std::to_string(l);
     spmv(d.P, e.z.p, z, nullptr, 2, s); // z += P zc
     smooth(c, l, r, z, opts.post_sweeps);
+    prof_tag() = saved;
 }
 
 void DevHierarchy::vcycle(Ctx& c, const double* r, double* z)

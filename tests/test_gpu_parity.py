@@ -29,11 +29,15 @@ def _csr(m):
     return api.Csr(m.nrows, m.ncols, m.rowptr, m.col, m.val)
 
 
-def _assert_history(h_gpu, h_ref):
+def _assert_history(h_gpu, h_ref, floor=0.0):
+    """Outer residual estimates within 1e-10 relative; `floor` is the
+    roundoff floor of a solve that converged to machine precision (estimates
+    below ~1e-13 of the right-hand side carry no information)."""
     n = min(len(h_gpu), len(h_ref))
     assert abs(len(h_gpu) - len(h_ref)) <= 1, (len(h_gpu), len(h_ref))
     for k in range(n):
-        assert abs(h_gpu[k] - h_ref[k]) <= HIST_TOL * h_ref[0] + HIST_TOL * abs(h_ref[k]), (k, h_gpu[k], h_ref[k])
+        tol = HIST_TOL * h_ref[0] + HIST_TOL * abs(h_ref[k]) + floor
+        assert abs(h_gpu[k] - h_ref[k]) <= tol, (k, h_gpu[k], h_ref[k])
 
 
 def _assert_stats(sg, sr):
@@ -231,7 +235,7 @@ def test_solve_block_system_random_saddle(oracle, nv, np_, seed, d_shift):
     assert sg["converged"] and sr["converged"]
     assert np.max(np.abs(xg - x_lu)) <= 1e-5 * np.linalg.norm(x_lu)
     _assert_stats(sg, sr)
-    _assert_history(hg, hr)
+    _assert_history(hg, hr, floor=1e-13 * np.linalg.norm(b))
     assert _rel(xg, xr) < X_TOL
 
 
