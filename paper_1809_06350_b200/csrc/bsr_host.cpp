@@ -3,6 +3,7 @@
 // mesh-static: built once per mesh (or per AMG level); only values move per
 // Newton step.
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 
 #include "ed_internal.hpp"
@@ -146,6 +147,22 @@ std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLay
     int widest = 0;
     for (int l = 0; l < nlev; ++l) widest = std::max(widest, S.lev_ptr[l + 1] - S.lev_ptr[l]);
     S.chain = static_cast<int64_t>(widest) * S.L <= 1024;
+    // narrow, deep schedules whose vector fits in a cluster's shared memory
+    // (<= 16 CTAs x 192 KB) run cluster-resident: z lives in DSMEM and a
+    // cluster barrier separates levels
+    S.avg_rows_per_level = nlev > 0 ? S.nbr / nlev : 0;
+    const int64_t zbytes = static_cast<int64_t>(S.nbr) * Rb * 8;
+    S.cluster = 0;
+    if (Rb == Cb && nlev > 1 && S.avg_rows_per_level <= 256 && std::getenv("ED_NO_CLUSTER") == nullptr) {
+        for (int cs = 1; cs <= 16; cs *= 2)
+            if (zbytes <= static_cast<int64_t>(cs) * 192 * 1024) {
+                S.cluster = cs;
+                break;
+            }
+        // enough lanes that a level's blocks spread to <= ~4 per thread
+        const double blocks_per_level = static_cast<double>(S.nnzb) / nlev;
+        while (S.cluster > 0 && S.cluster < 16 && blocks_per_level > 4.0 * 512 * S.cluster) S.cluster *= 2;
+    }
     ED_CUDA(cudaStreamSynchronize(s)); // host vectors die at return
     return st;
 }

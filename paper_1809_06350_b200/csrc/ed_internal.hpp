@@ -145,6 +145,8 @@ struct BsrStruct {
     DevArray<int> lev_items;  // [nlev] items per level
     DevArray<unsigned int> sync; // [nlev + 2]: per-level done counters, ticket
     bool chain = false;          // narrow levels: single-CTA sweep with CTA barriers
+    int cluster = 0;             // > 0: cluster-resident sweep over this many CTAs (z in DSMEM)
+    int avg_rows_per_level = 0;
     DevArray<int> d_lev_ptr;     // device copy of lev_ptr
     // host mirrors
     std::vector<int> h_rowptr, h_col, h_perm, h_inv;

@@ -11,6 +11,7 @@
 // take work items in level order from a ticket counter, prefetch their rows'
 // matrix data, wait on the previous level's completion counter, and publish
 // their own, so there is no launch (and no grid-wide barrier) per level.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -18,6 +19,8 @@
 #include "ed_internal.hpp"
 
 namespace edb {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -279,6 +282,132 @@ __global__ void __launch_bounds__(kThreads) k_sgs_flow(BsrArgs m, const double* 
     }
 }
 
+// One Gauss-Seidel half sweep over narrow, deep schedules with z resident
+// in the cluster's distributed shared memory: each CTA of the cluster holds
+// a slice of z; the rows of a level are dealt round-robin to the CTAs, each
+// row gets G lanes (a power of two sized so the level fills the CTA), lanes
+// gather z through DSMEM, the group leader solves the diagonal block in
+// sweep order and writes the new values to the owning CTA's slice (and to
+// global memory); a cluster barrier (release/acquire) separates levels.
+constexpr int kClT = 512;
+
+template <int B, bool FWD>
+__global__ void __launch_bounds__(kClT) k_sgs_cluster(BsrArgs m, const double* __restrict__ bvec, double* z,
+                                                      const double* __restrict__ invd,
+                                                      const int* __restrict__ lev_ptr, int nlev, int nsc, int slice)
+{
+    extern __shared__ double smem[];
+    double* zs = smem;                 // this CTA's slice of z
+    double* red = smem + slice;        // [kClT/32][B] cross-warp partials
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = static_cast<int>(cl.block_rank());
+    const int cs = static_cast<int>(cl.num_blocks());
+    const int tid = threadIdx.x;
+    for (int i = tid; i < slice; i += kClT) {
+        const int gi = rank * slice + i;
+        zs[i] = gi < nsc ? z[gi] : 0.0;
+    }
+    cl.sync();
+    auto zptr = [&](int gi) -> double* {
+        const int owner = gi / slice;
+        return cl.map_shared_rank(zs, owner) + (gi - owner * slice);
+    };
+    for (int li = 0; li < nlev; ++li) {
+        const int lev = FWD ? li : nlev - 1 - li;
+        const int r0 = lev_ptr[lev], r1 = lev_ptr[lev + 1];
+        const int R = r1 - r0;
+        const int myR = R > rank ? (R - rank + cs - 1) / cs : 0;
+        if (myR > 0) {
+            int G = kClT;
+            while (G > 1 && G * myR > kClT) G >>= 1;
+            const int rpp = kClT / G;
+            for (int q0 = 0; q0 < myR; q0 += rpp) {
+                const int q = q0 + tid / G;
+                const int lane = tid % G;
+                const bool valid = q < myR;
+                const int s = r0 + rank + q * cs;
+                int row = 0, kb = 0, ke = 0;
+                double bb[B], id[B], D[B * B];
+                if (valid) {
+                    row = m.perm ? m.perm[s] : s;
+                    kb = m.rowptr[s] + lane;
+                    ke = m.rowptr[s + 1];
+                    if (lane == 0) { // leader prefetches the z-independent diagonal data
+                        const int dp = m.dpos[s];
+#pragma unroll
+                        for (int d = 0; d < B; ++d) {
+                            bb[d] = bvec[static_cast<int64_t>(row) * B + d];
+                            id[d] = invd[static_cast<int64_t>(row) * B + d];
+                        }
+#pragma unroll
+                        for (int e = 0; e < B * B; ++e)
+                            D[e] = dp >= 0 ? __ldg(m.val + static_cast<int64_t>(dp) * (B * B) + e) : 0.0;
+                    }
+                }
+                double acc[B];
+#pragma unroll
+                for (int r = 0; r < B; ++r) acc[r] = 0.0;
+#pragma unroll 2
+                for (int k = kb; k < ke; k += G) {
+                    const int c = __ldg(m.col + k);
+                    if (c == row) continue;
+                    const double* vp = m.val + static_cast<int64_t>(k) * (B * B);
+#pragma unroll
+                    for (int d = 0; d < B; ++d) {
+                        const double zv = *zptr(c * B + d);
+#pragma unroll
+                        for (int r = 0; r < B; ++r) acc[r] = fma(__ldg(vp + r * B + d), zv, acc[r]);
+                    }
+                }
+                if (G <= 32) {
+#pragma unroll
+                    for (int r = 0; r < B; ++r)
+                        for (int o = G / 2; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o, G);
+                } else {
+#pragma unroll
+                    for (int r = 0; r < B; ++r)
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+                    if ((tid & 31) == 0)
+#pragma unroll
+                        for (int r = 0; r < B; ++r) red[(tid >> 5) * B + r] = acc[r];
+                    __syncthreads();
+                    if (lane == 0) {
+                        const int w0 = tid >> 5;
+#pragma unroll
+                        for (int r = 0; r < B; ++r) {
+                            double t = 0.0;
+                            for (int ww = 0; ww < G / 32; ++ww) t += red[(w0 + ww) * B + r];
+                            acc[r] = t;
+                        }
+                    }
+                    __syncthreads();
+                }
+                if (valid && lane == 0) {
+                    double zv[B];
+#pragma unroll
+                    for (int d = 0; d < B; ++d) zv[d] = *zptr(row * B + d);
+#pragma unroll
+                    for (int ci = 0; ci < B; ++ci) {
+                        const int c = FWD ? ci : B - 1 - ci;
+                        double a = bb[c] - acc[c];
+#pragma unroll
+                        for (int d = 0; d < B; ++d)
+                            if (d != c) a -= D[c * B + d] * zv[d];
+                        zv[c] = a * id[c];
+                    }
+#pragma unroll
+                    for (int d = 0; d < B; ++d) {
+                        *zptr(row * B + d) = zv[d];
+                        z[static_cast<int64_t>(row) * B + d] = zv[d];
+                    }
+                }
+            }
+        }
+        cl.sync();
+    }
+}
+
 // One Gauss-Seidel half sweep over narrow levels: a single CTA walks the
 // levels with a CTA barrier between them (no global atomics or polling).
 template <int B, int L, bool FWD>
@@ -407,6 +536,35 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
     if (S.nitems == 0) return;
     const int nlev = S.nlev();
     const BsrArgs a = args_of(A);
+    if (S.cluster > 0) {
+        const int nsc = S.nbr * B;
+        const int cs = S.cluster;
+        const int slice = (nsc + cs - 1) / cs;
+        const size_t smem = (static_cast<size_t>(slice) + (kClT / 32) * B) * sizeof(double);
+        auto kern = fwd ? k_sgs_cluster<B, true> : k_sgs_cluster<B, false>;
+        static bool attr_done[2][2] = {{false, false}, {false, false}};
+        bool& done = attr_done[B == 3][fwd ? 1 : 0];
+        if (!done) {
+            ED_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            ED_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            done = true;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cs, 1, 1);
+        cfg.blockDim = dim3(kClT, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cs;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        ED_CUDA(cudaLaunchKernelEx(&cfg, kern, a, b, z, invd, S.d_lev_ptr.p, nlev, nsc, slice));
+        after_launch("k_sgs_cluster");
+        return;
+    }
     if (S.chain) {
         ED_LANES(S.L, {
             if (fwd)
