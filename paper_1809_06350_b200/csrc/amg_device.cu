@@ -285,6 +285,93 @@ __global__ void k_spgemm_numeric(const int* __restrict__ arp, const int* __restr
     }
 }
 
+// ---- warp-per-row variants for long rows (coarse, dense RAP levels) -------
+__global__ void k_cand_fill_warp(const int* __restrict__ arp, const int* __restrict__ acol,
+                                 const int* __restrict__ brp, const int* __restrict__ bcol, int r0, int r1,
+                                 const int* __restrict__ seg, int* keys)
+{
+    const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int I = r0 + static_cast<int>(w);
+    if (I >= r1) return;
+    int o = seg[I - r0];
+    for (int k = arp[I]; k < arp[I + 1]; ++k) {
+        const int K = acol[k];
+        const int b0 = brp[K], b1 = brp[K + 1];
+        for (int kb = b0 + lane; kb < b1; kb += 32) keys[o + kb - b0] = bcol[kb];
+        o += b1 - b0;
+    }
+}
+
+__global__ void k_unique_count_warp(const int* __restrict__ keys, const int* __restrict__ seg, int nseg, int* ucnt)
+{
+    const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nseg) return;
+    const int a = seg[w], b = seg[w + 1];
+    int c = 0;
+    for (int k = a + lane; k < b; k += 32) c += (k == a || keys[k] != keys[k - 1]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) ucnt[w] = c;
+}
+
+__global__ void k_unique_write_warp(const int* __restrict__ keys, const int* __restrict__ seg, int nseg,
+                                    const int* __restrict__ uoff, int* out)
+{
+    const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nseg) return;
+    const int a = seg[w], b = seg[w + 1];
+    int o = uoff[w];
+    for (int base = a; base < b; base += 32) {
+        const int k = base + lane;
+        const bool first = k < b && (k == a || keys[k] != keys[k - 1]);
+        const unsigned m = __ballot_sync(0xffffffffu, first);
+        if (first) out[o + __popc(m & ((1u << lane) - 1u))] = keys[k];
+        o += __popc(m);
+    }
+}
+
+// One warp per scalar row (I, c): the A row is walked in order (K, d); the
+// entries of B row K are split across lanes (distinct C columns inside one B
+// row), and __syncwarp orders consecutive K steps, so every C entry still
+// receives its products in csr_matmul's traversal order.
+template <int RA, int KA, int CB>
+__global__ void k_spgemm_numeric_warp(const int* __restrict__ arp, const int* __restrict__ acol,
+                                      const double* __restrict__ aval, const int* __restrict__ brp,
+                                      const int* __restrict__ bcol, const double* __restrict__ bval,
+                                      const int* __restrict__ crp, const int* __restrict__ ccol, double* cval, int n)
+{
+    const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int I = static_cast<int>(w / RA), c = static_cast<int>(w % RA);
+    if (I >= n) return;
+    const int c0 = crp[I], c1 = crp[I + 1];
+    for (int k = arp[I]; k < arp[I + 1]; ++k) {
+        const int K = acol[k];
+        const int b0 = brp[K], b1 = brp[K + 1];
+        for (int kb = b0 + lane; kb < b1; kb += 32) {
+            const int J = bcol[kb];
+            int lo = c0, hi = c1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (ccol[mid] < J) lo = mid + 1;
+                else hi = mid;
+            }
+            double* cv = cval + static_cast<int64_t>(lo) * RA * CB + c * CB;
+#pragma unroll
+            for (int d = 0; d < KA; ++d) {
+                const double a = aval[static_cast<int64_t>(k) * RA * KA + c * KA + d];
+                const double* bv = bval + static_cast<int64_t>(kb) * KA * CB + d * CB;
+#pragma unroll
+                for (int e = 0; e < CB; ++e) cv[e] = __dadd_rn(cv[e], __dmul_rn(a, bv[e]));
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // ---- csr_add (csr.cpp:168-198) on block rows -------------------------------
 __global__ void k_add_count(const int* __restrict__ arp, const int* __restrict__ acol, const int* __restrict__ brp,
                             const int* __restrict__ bcol, int n, int* cnt)
@@ -449,7 +536,12 @@ DBsr spgemm(const DBsr& A, const DBsr& B, cudaStream_t s)
         DevArray<int> dseg;
         dseg.upload(seg, s);
         DevArray<int> keys(std::max<int64_t>(tot, 1)), sorted(std::max<int64_t>(tot, 1));
-        k_cand_fill<<<g1(nseg), kT, 0, s>>>(A.rowptr.p, A.col.p, B.rowptr.p, B.col.p, r0, r1, dseg.p, keys.p);
+        const bool wide = tot > 256LL * nseg; // long rows: a warp per row
+        if (wide)
+            k_cand_fill_warp<<<g1(32LL * nseg), kT, 0, s>>>(A.rowptr.p, A.col.p, B.rowptr.p, B.col.p, r0, r1, dseg.p,
+                                                           keys.p);
+        else
+            k_cand_fill<<<g1(nseg), kT, 0, s>>>(A.rowptr.p, A.col.p, B.rowptr.p, B.col.p, r0, r1, dseg.p, keys.p);
         after_launch("k_cand_fill");
         size_t tb = 0;
         cub::DeviceSegmentedSort::SortKeys(nullptr, tb, keys.p, sorted.p, static_cast<int>(tot), nseg, dseg.p,
@@ -460,7 +552,10 @@ DBsr spgemm(const DBsr& A, const DBsr& B, cudaStream_t s)
         after_launch("cub_segmented_sort");
         keys.release();
         DevArray<int> uc(nseg);
-        k_unique_count<<<g1(nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, uc.p);
+        if (wide)
+            k_unique_count_warp<<<g1(32LL * nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, uc.p);
+        else
+            k_unique_count<<<g1(nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, uc.p);
         after_launch("k_unique_count");
         const std::vector<int> huc = uc.to_host(s);
         std::vector<int> uoff;
@@ -468,7 +563,10 @@ DBsr spgemm(const DBsr& A, const DBsr& B, cudaStream_t s)
         DevArray<int> duoff;
         duoff.upload(uoff, s);
         DevArray<int> cols(std::max(uoff[nseg], 1));
-        k_unique_write<<<g1(nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, duoff.p, cols.p);
+        if (wide)
+            k_unique_write_warp<<<g1(32LL * nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, duoff.p, cols.p);
+        else
+            k_unique_write<<<g1(nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, duoff.p, cols.p);
         after_launch("k_unique_write");
         for (int i = 0; i < nseg; ++i) ucnt_all[r0 + i] = huc[i];
         chunk_tot.push_back(uoff[nseg]);
@@ -491,14 +589,28 @@ DBsr spgemm(const DBsr& A, const DBsr& B, cudaStream_t s)
     C.val.alloc(std::max<int64_t>(C.nnzb * E, 1));
     C.val.zero(s);
     const int64_t threads = static_cast<int64_t>(n) * A.Rb;
-    if (A.Rb == 3 && A.Cb == 3 && B.Cb == 3)
-        k_spgemm_numeric<3, 3, 3><<<g1(threads), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, B.rowptr.p, B.col.p,
-                                                             B.val.p, C.rowptr.p, C.col.p, C.val.p, n);
-    else if (A.Rb == 1 && A.Cb == 1 && B.Cb == 1)
-        k_spgemm_numeric<1, 1, 1><<<g1(threads), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, B.rowptr.p, B.col.p,
-                                                             B.val.p, C.rowptr.p, C.col.p, C.val.p, n);
-    else
+    int64_t tot_cand = 0;
+    for (const int64_t v : hc) tot_cand += v;
+    const bool wide_rows = tot_cand > 256LL * std::max(n, 1);
+    if (A.Rb == 3 && A.Cb == 3 && B.Cb == 3) {
+        if (wide_rows)
+            k_spgemm_numeric_warp<3, 3, 3><<<g1(32 * threads), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, B.rowptr.p,
+                                                                          B.col.p, B.val.p, C.rowptr.p, C.col.p,
+                                                                          C.val.p, n);
+        else
+            k_spgemm_numeric<3, 3, 3><<<g1(threads), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, B.rowptr.p, B.col.p,
+                                                                 B.val.p, C.rowptr.p, C.col.p, C.val.p, n);
+    } else if (A.Rb == 1 && A.Cb == 1 && B.Cb == 1) {
+        if (wide_rows)
+            k_spgemm_numeric_warp<1, 1, 1><<<g1(32 * threads), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, B.rowptr.p,
+                                                                          B.col.p, B.val.p, C.rowptr.p, C.col.p,
+                                                                          C.val.p, n);
+        else
+            k_spgemm_numeric<1, 1, 1><<<g1(threads), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, B.rowptr.p, B.col.p,
+                                                                 B.val.p, C.rowptr.p, C.col.p, C.val.p, n);
+    } else {
         throw Error(ED_UNSUPPORTED, "spgemm: unsupported block shape");
+    }
     after_launch("k_spgemm_numeric");
     ED_CUDA(cudaStreamSynchronize(s));
     return C;

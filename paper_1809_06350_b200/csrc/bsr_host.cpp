@@ -153,7 +153,7 @@ std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLay
     S.avg_rows_per_level = nlev > 0 ? S.nbr / nlev : 0;
     const int64_t zbytes = static_cast<int64_t>(S.nbr) * Rb * 8;
     S.cluster = 0;
-    if (Rb == Cb && nlev > 1 && S.avg_rows_per_level <= 256 && std::getenv("ED_NO_CLUSTER") == nullptr) {
+    if (Rb == Cb && nlev > 1 && S.avg_rows_per_level <= 32 && std::getenv("ED_NO_CLUSTER") == nullptr) {
         for (int cs = 1; cs <= 16; cs *= 2)
             if (zbytes <= static_cast<int64_t>(cs) * 192 * 1024) {
                 S.cluster = cs;

@@ -282,23 +282,76 @@ __global__ void __launch_bounds__(kThreads) k_sgs_flow(BsrArgs m, const double* 
     }
 }
 
-// One Gauss-Seidel half sweep over narrow, deep schedules with z resident
-// in the cluster's distributed shared memory: each CTA of the cluster holds
-// a slice of z; the rows of a level are dealt round-robin to the CTAs, each
-// row gets G lanes (a power of two sized so the level fills the CTA), lanes
-// gather z through DSMEM, the group leader solves the diagonal block in
-// sweep order and writes the new values to the owning CTA's slice (and to
-// global memory); a cluster barrier (release/acquire) separates levels.
 constexpr int kClT = 512;
+constexpr int kPFB = 3; // blocks per lane prefetched ahead of the level barrier
 
+template <int B>
+struct ClRow {
+    int s, row, kb, ke, lane, G;
+    bool valid;
+    int c[kPFB];
+    double v[kPFB][B * B];
+    double bb[B], id[B], D[B * B];
+};
+
+// Rows of level `lev` dealt to this CTA: q = q0 + tid / G (q < myR).  Loads
+// everything that does not depend on z: the lane's first kPFB blocks, and for
+// the group leader b, inv_diag and the diagonal block.
+template <int B>
+__device__ __forceinline__ void cl_prefetch(const BsrArgs& m, const double* __restrict__ bvec,
+                                            const double* __restrict__ invd, const int* __restrict__ lev_ptr, int lev,
+                                            int rank, int cs, int tid, int q0, ClRow<B>& P)
+{
+    const int r0 = lev_ptr[lev], R = lev_ptr[lev + 1] - r0;
+    const int myR = R > rank ? (R - rank + cs - 1) / cs : 0;
+    int G = kClT;
+    while (G > 1 && G * myR > kClT) G >>= 1;
+    P.G = G;
+    const int q = q0 + tid / G;
+    P.lane = tid % G;
+    P.valid = q < myR;
+    P.s = r0 + rank + q * cs;
+    P.row = P.valid ? (m.perm ? m.perm[P.s] : P.s) : 0;
+    P.kb = P.valid ? m.rowptr[P.s] + P.lane : 0;
+    P.ke = P.valid ? m.rowptr[P.s + 1] : 0;
+#pragma unroll
+    for (int j = 0; j < kPFB; ++j) {
+        const int k = P.kb + j * G;
+        P.c[j] = k < P.ke ? __ldg(m.col + k) : -1;
+        if (k < P.ke) {
+#pragma unroll
+            for (int e = 0; e < B * B; ++e) P.v[j][e] = __ldg(m.val + static_cast<int64_t>(k) * (B * B) + e);
+        }
+    }
+    if (P.valid && P.lane == 0) {
+        const int dp = m.dpos[P.s];
+#pragma unroll
+        for (int d = 0; d < B; ++d) {
+            P.bb[d] = bvec[static_cast<int64_t>(P.row) * B + d];
+            P.id[d] = invd[static_cast<int64_t>(P.row) * B + d];
+        }
+#pragma unroll
+        for (int e = 0; e < B * B; ++e) P.D[e] = dp >= 0 ? __ldg(m.val + static_cast<int64_t>(dp) * (B * B) + e) : 0.0;
+    }
+}
+
+// Gauss-Seidel half sweep over narrow, deep schedules with z resident in
+// the cluster's distributed shared memory: each CTA holds a slice of z; the
+// rows of a level are dealt round-robin to the CTAs, each row gets G lanes (a
+// power of two sized so the level fills the CTA), lanes gather z through
+// DSMEM, the group leader solves the diagonal block in sweep order and writes
+// the new values to the owning slice (and to global memory); a cluster
+// barrier (release/acquire) separates levels.  The next level's matrix data
+// is loaded before the barrier, so only DSMEM gathers sit on the critical
+// path of a level.
 template <int B, bool FWD>
 __global__ void __launch_bounds__(kClT) k_sgs_cluster(BsrArgs m, const double* __restrict__ bvec, double* z,
                                                       const double* __restrict__ invd,
                                                       const int* __restrict__ lev_ptr, int nlev, int nsc, int slice)
 {
     extern __shared__ double smem[];
-    double* zs = smem;                 // this CTA's slice of z
-    double* red = smem + slice;        // [kClT/32][B] cross-warp partials
+    double* zs = smem;          // this CTA's slice of z
+    double* red = smem + slice; // [kClT/32][B] cross-warp partials
     cg::cluster_group cl = cg::this_cluster();
     const int rank = static_cast<int>(cl.block_rank());
     const int cs = static_cast<int>(cl.num_blocks());
@@ -307,106 +360,96 @@ __global__ void __launch_bounds__(kClT) k_sgs_cluster(BsrArgs m, const double* _
         const int gi = rank * slice + i;
         zs[i] = gi < nsc ? z[gi] : 0.0;
     }
-    cl.sync();
     auto zptr = [&](int gi) -> double* {
         const int owner = gi / slice;
         return cl.map_shared_rank(zs, owner) + (gi - owner * slice);
     };
+    ClRow<B> P;
+    cl_prefetch<B>(m, bvec, invd, lev_ptr, FWD ? 0 : nlev - 1, rank, cs, tid, 0, P);
+    cl.sync();
     for (int li = 0; li < nlev; ++li) {
         const int lev = FWD ? li : nlev - 1 - li;
-        const int r0 = lev_ptr[lev], r1 = lev_ptr[lev + 1];
-        const int R = r1 - r0;
+        const int R = lev_ptr[lev + 1] - lev_ptr[lev];
         const int myR = R > rank ? (R - rank + cs - 1) / cs : 0;
-        if (myR > 0) {
-            int G = kClT;
-            while (G > 1 && G * myR > kClT) G >>= 1;
-            const int rpp = kClT / G;
-            for (int q0 = 0; q0 < myR; q0 += rpp) {
-                const int q = q0 + tid / G;
-                const int lane = tid % G;
-                const bool valid = q < myR;
-                const int s = r0 + rank + q * cs;
-                int row = 0, kb = 0, ke = 0;
-                double bb[B], id[B], D[B * B];
-                if (valid) {
-                    row = m.perm ? m.perm[s] : s;
-                    kb = m.rowptr[s] + lane;
-                    ke = m.rowptr[s + 1];
-                    if (lane == 0) { // leader prefetches the z-independent diagonal data
-                        const int dp = m.dpos[s];
+        const int rpp = kClT / P.G;
+        for (int q0 = 0; q0 < myR; q0 += rpp) {
+            if (q0 > 0) cl_prefetch<B>(m, bvec, invd, lev_ptr, lev, rank, cs, tid, q0, P);
+            const int G = P.G;
+            double acc[B];
 #pragma unroll
-                        for (int d = 0; d < B; ++d) {
-                            bb[d] = bvec[static_cast<int64_t>(row) * B + d];
-                            id[d] = invd[static_cast<int64_t>(row) * B + d];
-                        }
+            for (int r = 0; r < B; ++r) acc[r] = 0.0;
 #pragma unroll
-                        for (int e = 0; e < B * B; ++e)
-                            D[e] = dp >= 0 ? __ldg(m.val + static_cast<int64_t>(dp) * (B * B) + e) : 0.0;
-                    }
-                }
-                double acc[B];
-#pragma unroll
-                for (int r = 0; r < B; ++r) acc[r] = 0.0;
-#pragma unroll 2
-                for (int k = kb; k < ke; k += G) {
-                    const int c = __ldg(m.col + k);
-                    if (c == row) continue;
-                    const double* vp = m.val + static_cast<int64_t>(k) * (B * B);
+            for (int j = 0; j < kPFB; ++j) {
+                const int c = P.c[j];
+                if (c >= 0 && c != P.row) {
 #pragma unroll
                     for (int d = 0; d < B; ++d) {
                         const double zv = *zptr(c * B + d);
 #pragma unroll
-                        for (int r = 0; r < B; ++r) acc[r] = fma(__ldg(vp + r * B + d), zv, acc[r]);
-                    }
-                }
-                if (G <= 32) {
-#pragma unroll
-                    for (int r = 0; r < B; ++r)
-                        for (int o = G / 2; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o, G);
-                } else {
-#pragma unroll
-                    for (int r = 0; r < B; ++r)
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
-                    if ((tid & 31) == 0)
-#pragma unroll
-                        for (int r = 0; r < B; ++r) red[(tid >> 5) * B + r] = acc[r];
-                    __syncthreads();
-                    if (lane == 0) {
-                        const int w0 = tid >> 5;
-#pragma unroll
-                        for (int r = 0; r < B; ++r) {
-                            double t = 0.0;
-                            for (int ww = 0; ww < G / 32; ++ww) t += red[(w0 + ww) * B + r];
-                            acc[r] = t;
-                        }
-                    }
-                    __syncthreads();
-                }
-                if (valid && lane == 0) {
-                    double zv[B];
-#pragma unroll
-                    for (int d = 0; d < B; ++d) zv[d] = *zptr(row * B + d);
-#pragma unroll
-                    for (int ci = 0; ci < B; ++ci) {
-                        const int c = FWD ? ci : B - 1 - ci;
-                        double a = bb[c] - acc[c];
-#pragma unroll
-                        for (int d = 0; d < B; ++d)
-                            if (d != c) a -= D[c * B + d] * zv[d];
-                        zv[c] = a * id[c];
-                    }
-#pragma unroll
-                    for (int d = 0; d < B; ++d) {
-                        *zptr(row * B + d) = zv[d];
-                        z[static_cast<int64_t>(row) * B + d] = zv[d];
+                        for (int r = 0; r < B; ++r) acc[r] = fma(P.v[j][r * B + d], zv, acc[r]);
                     }
                 }
             }
+            for (int k = P.kb + kPFB * G; k < P.ke; k += G) {
+                const int c = __ldg(m.col + k);
+                if (c == P.row) continue;
+                const double* vp = m.val + static_cast<int64_t>(k) * (B * B);
+#pragma unroll
+                for (int d = 0; d < B; ++d) {
+                    const double zv = *zptr(c * B + d);
+#pragma unroll
+                    for (int r = 0; r < B; ++r) acc[r] = fma(__ldg(vp + r * B + d), zv, acc[r]);
+                }
+            }
+            if (G <= 32) {
+#pragma unroll
+                for (int r = 0; r < B; ++r)
+                    for (int o = G / 2; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o, G);
+            } else {
+#pragma unroll
+                for (int r = 0; r < B; ++r)
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+                if ((tid & 31) == 0)
+#pragma unroll
+                    for (int r = 0; r < B; ++r) red[(tid >> 5) * B + r] = acc[r];
+                __syncthreads();
+                if (P.lane == 0) {
+                    const int w0 = tid >> 5;
+#pragma unroll
+                    for (int r = 0; r < B; ++r) {
+                        double t = 0.0;
+                        for (int ww = 0; ww < G / 32; ++ww) t += red[(w0 + ww) * B + r];
+                        acc[r] = t;
+                    }
+                }
+                __syncthreads();
+            }
+            if (P.valid && P.lane == 0) {
+                double zv[B];
+#pragma unroll
+                for (int d = 0; d < B; ++d) zv[d] = *zptr(P.row * B + d);
+#pragma unroll
+                for (int ci = 0; ci < B; ++ci) {
+                    const int c = FWD ? ci : B - 1 - ci;
+                    double a = P.bb[c] - acc[c];
+#pragma unroll
+                    for (int d = 0; d < B; ++d)
+                        if (d != c) a -= P.D[c * B + d] * zv[d];
+                    zv[c] = a * P.id[c];
+                }
+#pragma unroll
+                for (int d = 0; d < B; ++d) {
+                    *zptr(P.row * B + d) = zv[d];
+                    z[static_cast<int64_t>(P.row) * B + d] = zv[d];
+                }
+            }
         }
+        if (li + 1 < nlev) cl_prefetch<B>(m, bvec, invd, lev_ptr, FWD ? li + 1 : nlev - 2 - li, rank, cs, tid, 0, P);
         cl.sync();
     }
 }
+
 
 // One Gauss-Seidel half sweep over narrow levels: a single CTA walks the
 // levels with a CTA barrier between them (no global atomics or polling).
