@@ -344,7 +344,11 @@ __device__ __forceinline__ void cl_prefetch(const BsrArgs& m, const double* __re
 // barrier (release/acquire) separates levels.  The next level's matrix data
 // is loaded before the barrier, so only DSMEM gathers sit on the critical
 // path of a level.
-template <int B, bool FWD>
+__device__ __forceinline__ void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait_acquire() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+
+template <int B, bool FWD, bool MULTI>
 __global__ void __launch_bounds__(kClT) k_sgs_cluster(BsrArgs m, const double* __restrict__ bvec, double* z,
                                                       const double* __restrict__ invd,
                                                       const int* __restrict__ lev_ptr, int nlev, int nsc, int slice)
@@ -361,12 +365,14 @@ __global__ void __launch_bounds__(kClT) k_sgs_cluster(BsrArgs m, const double* _
         zs[i] = gi < nsc ? z[gi] : 0.0;
     }
     auto zptr = [&](int gi) -> double* {
+        if (!MULTI) return zs + gi;
         const int owner = gi / slice;
         return cl.map_shared_rank(zs, owner) + (gi - owner * slice);
     };
     ClRow<B> P;
     cl_prefetch<B>(m, bvec, invd, lev_ptr, FWD ? 0 : nlev - 1, rank, cs, tid, 0, P);
-    cl.sync();
+    if (MULTI) cl.sync();
+    else __syncthreads();
     for (int li = 0; li < nlev; ++li) {
         const int lev = FWD ? li : nlev - 1 - li;
         const int R = lev_ptr[lev + 1] - lev_ptr[lev];
@@ -439,15 +445,25 @@ __global__ void __launch_bounds__(kClT) k_sgs_cluster(BsrArgs m, const double* _
                     zv[c] = a * P.id[c];
                 }
 #pragma unroll
-                for (int d = 0; d < B; ++d) {
-                    *zptr(P.row * B + d) = zv[d];
-                    z[static_cast<int64_t>(P.row) * B + d] = zv[d];
-                }
+                for (int d = 0; d < B; ++d) *zptr(P.row * B + d) = zv[d];
+                if (MULTI) fence_cluster(); // only writers pay the release fence
             }
         }
-        if (li + 1 < nlev) cl_prefetch<B>(m, bvec, invd, lev_ptr, FWD ? li + 1 : nlev - 2 - li, rank, cs, tid, 0, P);
-        cl.sync();
+        if (MULTI) {
+            cluster_arrive_relaxed();
+            if (li + 1 < nlev) cl_prefetch<B>(m, bvec, invd, lev_ptr, FWD ? li + 1 : nlev - 2 - li, rank, cs, tid, 0, P);
+            cluster_wait_acquire();
+        } else {
+            if (li + 1 < nlev) cl_prefetch<B>(m, bvec, invd, lev_ptr, FWD ? li + 1 : nlev - 2 - li, rank, cs, tid, 0, P);
+            __syncthreads();
+        }
     }
+    // slices back to global memory
+    for (int i = tid; i < slice; i += kClT) {
+        const int gi = rank * slice + i;
+        if (gi < nsc) z[gi] = zs[i];
+    }
+    if (MULTI) cl.sync(); // keep remote slices alive until every CTA is done
 }
 
 
@@ -584,9 +600,10 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
         const int cs = S.cluster;
         const int slice = (nsc + cs - 1) / cs;
         const size_t smem = (static_cast<size_t>(slice) + (kClT / 32) * B) * sizeof(double);
-        auto kern = fwd ? k_sgs_cluster<B, true> : k_sgs_cluster<B, false>;
-        static bool attr_done[2][2] = {{false, false}, {false, false}};
-        bool& done = attr_done[B == 3][fwd ? 1 : 0];
+        auto kern = cs > 1 ? (fwd ? k_sgs_cluster<B, true, true> : k_sgs_cluster<B, false, true>)
+                           : (fwd ? k_sgs_cluster<B, true, false> : k_sgs_cluster<B, false, false>);
+        static bool attr_done[2][2][2] = {};
+        bool& done = attr_done[B == 3][fwd ? 1 : 0][cs > 1 ? 1 : 0];
         if (!done) {
             ED_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
             ED_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
