@@ -761,6 +761,10 @@ Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s)
     const BsrLayout lay = make_layout(pat, order, lvl);
     out.st = bsr_make_struct(pat, lay, m.Rb, m.Cb, s);
     out.st->leveled = true;
+    if (std::getenv("ED_AMG_VERBOSE"))
+        std::fprintf(stderr, "[amg-dev] level op: block rows %d blocks %lld gs-levels %d lanes %d cluster %d chain %d\n",
+                     m.nbr, static_cast<long long>(m.nnzb), out.st->nlev(), out.st->L, out.st->cluster,
+                     out.st->chain ? 1 : 0);
     const int E = m.Rb * m.Cb;
     out.val.alloc(std::max<int64_t>(m.nnzb * E, 1));
     k_gather_rows<<<g1(m.nbr), kT, 0, s>>>(m.rowptr.p, m.val.p, out.st->perm.p ? out.st->perm.p : nullptr, m.nbr, E,

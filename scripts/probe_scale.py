@@ -12,6 +12,10 @@ for n in [int(a) for a in sys.argv[1:]] or [40]:
     st = cp.seeded_state()
     ctx.set_state(st)
     opts = cp.solver_options()
+    mx = int(os.environ.get("MAXIT", "0"))
+    if mx:  # profiling only: cap every Krylov solve
+        for c in (opts.outer, opts.a, opts.s, opts.inner):
+            c.max_iters = min(c.max_iters, mx)
     for rep in range(int(os.environ.get("REPS", "2"))):
         t = time.time(); out = ctx.newton_first_pass(cp.ts, opts); t_pass = time.time() - t
         ctx.set_state(st)
