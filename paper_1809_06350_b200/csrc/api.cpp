@@ -43,7 +43,9 @@ void after_launch(const char* what)
     const cudaError_t e = cudaPeekAtLastError();
     if (e != cudaSuccess) throw Error(ED_CUDA_ERROR, std::string("launch ") + what + ": " + cudaGetErrorString(e));
     if (g_prof.on) {
-        cudaDeviceSynchronize();
+        const cudaError_t e2 = cudaDeviceSynchronize();
+        if (e2 != cudaSuccess)
+            throw Error(ED_CUDA_ERROR, std::string("kernel ") + what + " failed: " + cudaGetErrorString(e2));
         const auto now = std::chrono::steady_clock::now();
         auto& slot = g_prof.t[prof_tag().empty() ? std::string(what) : std::string(what) + "@" + prof_tag()];
         slot.first += 1;
