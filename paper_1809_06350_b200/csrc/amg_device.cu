@@ -120,7 +120,7 @@ __global__ void k_symmetrize(const int* __restrict__ rowptr, const int* __restri
             if (!s) {
                 int lo = rowptr[J], hi = rowptr[J + 1];
                 while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
+                    const int mid = lo + ((hi - lo) >> 1);
                     if (col[mid] < I) lo = mid + 1;
                     else hi = mid;
                 }
@@ -265,7 +265,7 @@ __global__ void k_spgemm_numeric(const int* __restrict__ arp, const int* __restr
         int lo = c0, hi = c1;
         const int j0 = bcol[b0];
         while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
+            const int mid = lo + ((hi - lo) >> 1);
             if (ccol[mid] < j0) lo = mid + 1;
             else hi = mid;
         }
@@ -355,7 +355,7 @@ __global__ void k_spgemm_numeric_warp(const int* __restrict__ arp, const int* __
             const int J = bcol[kb];
             int lo = c0, hi = c1;
             while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
+                const int mid = lo + ((hi - lo) >> 1);
                 if (ccol[mid] < J) lo = mid + 1;
                 else hi = mid;
             }
