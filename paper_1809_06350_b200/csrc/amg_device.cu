@@ -747,6 +747,7 @@ Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s)
         return out;
     }
     // level schedule needs the pattern on the host
+    const double t_start = now_ms_host();
     BlockPattern pat;
     pat.nbr = m.nbr;
     pat.nbc = m.nbc;
@@ -762,9 +763,11 @@ Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s)
     out.st = bsr_make_struct(pat, lay, m.Rb, m.Cb, s);
     out.st->leveled = true;
     if (std::getenv("ED_AMG_VERBOSE"))
-        std::fprintf(stderr, "[amg-dev] level op: block rows %d blocks %lld gs-levels %d lanes %d cluster %d chain %d\n",
+        std::fprintf(stderr,
+                     "[amg-dev] level op: block rows %d blocks %lld gs-levels %d lanes %d cluster %d blocked %d "
+                     "(%.1f ms host)\n",
                      m.nbr, static_cast<long long>(m.nnzb), out.st->nlev(), out.st->L, out.st->cluster,
-                     out.st->chain ? 1 : 0);
+                     out.st->blocked ? out.st->ngroups : 0, now_ms_host() - t_start);
     const int E = m.Rb * m.Cb;
     out.val.alloc(std::max<int64_t>(m.nnzb * E, 1));
     k_gather_rows<<<g1(m.nbr), kT, 0, s>>>(m.rowptr.p, m.val.p, out.st->perm.p ? out.st->perm.p : nullptr, m.nbr, E,
@@ -940,6 +943,7 @@ DevSetupResult amg_build_device(const Bsr& A0, const AmgOpts& opts, cudaStream_t
         for (int64_t kk = Ah.rowptr[r]; kk < Ah.rowptr[r + 1]; ++kk)
             dense[static_cast<size_t>(Ah.col[kk]) * nr + r] = Ah.val[kk];
     res.pinv = cod_pinv(dense, nr, 1e-12);
+    if (std::getenv("ED_AMG_VERBOSE")) std::fprintf(stderr, "[amg-dev] alloc/free host ms so far: %.1f\n", alloc_ms());
     res.nc = nr;
     L.A = std::move(A);
     res.levels.push_back(std::move(L));

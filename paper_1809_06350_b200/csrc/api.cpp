@@ -56,6 +56,23 @@ void after_launch(const char* what)
 
 int64_t launch_count() { return g_launches.load(); }
 
+cudaStream_t& alloc_stream()
+{
+    static thread_local cudaStream_t s = nullptr;
+    return s;
+}
+
+double& alloc_ms()
+{
+    static double t = 0.0;
+    return t;
+}
+
+double now_ms_host()
+{
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 std::string& prof_tag()
 {
     static std::string t;
@@ -65,7 +82,13 @@ std::string& prof_tag()
 Ctx::Ctx(int dev) : device(dev)
 {
     ED_CUDA(cudaSetDevice(dev));
-    ED_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    ED_CUDA(cudaStreamCreateWithFlags(&owner.s, cudaStreamNonBlocking));
+    stream = owner.s;
+    // keep freed pool memory for the next Newton step's AMG rebuild
+    cudaMemPool_t pool;
+    ED_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = UINT64_MAX;
+    ED_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     host_buf(1024);
     dscratch_i.alloc(4);
     red.ensure(8, stream);
@@ -78,7 +101,7 @@ Ctx::~Ctx()
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (pinned) cudaFreeHost(pinned);
-    if (stream) cudaStreamDestroy(stream);
+    // the stream itself outlives every member array (StreamOwner is the first member)
 }
 
 double* Ctx::host_buf(size_t n)
@@ -241,6 +264,11 @@ template <class F>
 int guarded(ed_ctx* h, F&& f)
 {
     if (!h) return ED_INVALID_ARGUMENT;
+    struct StreamScope {
+        cudaStream_t prev;
+        explicit StreamScope(cudaStream_t s) : prev(alloc_stream()) { alloc_stream() = s; }
+        ~StreamScope() { alloc_stream() = prev; }
+    } scope(h->c.stream);
     try {
         f(h->c);
         h->c.err.clear();
@@ -886,7 +914,9 @@ int ed_bench_kernels(ed_ctx* ctx, const ed_block_solver_options* opts, int n_rep
                  2.0 * 8.0 * (static_cast<double>(S.nv) + S.np) + 4.0 * (S.A.st->nbr + S.C.st->nbr + 2);
         out[2] = time([&] { spmv(W.A, x.p, y.p, nullptr, 0, c.stream); });
         out[3] = W.A.bytes_per_spmv();
-        out[4] = time([&] { sgs_sweep(W.A, x.p, y.p, invd.p, true, c.stream); });
+        DevArray<double> gd;
+        blocked_dense(W.A, gd, c.stream);
+        out[4] = time([&] { sgs_sweep(W.A, x.p, y.p, invd.p, true, c.stream, gd.p); });
         // values+indices once, plus b and inv_diag read, z read+written
         out[5] = W.A.st->nnzb * (8.0 * W.Bv * W.Bv + 4.0) + 4.0 * (W.A.st->nbr + 1) + 4.0 * 8.0 * nv;
         out[6] = time([&] { spmv(W.S, x.p, y.p, nullptr, 0, c.stream); });

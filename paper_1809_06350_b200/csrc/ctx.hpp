@@ -86,6 +86,7 @@ struct DevLevel {
     const Bsr* A = nullptr; // level operator (fine: borrowed)
     Bsr Aown, P, R;
     DevArray<double> invd, r, z, s; // r/z for coarse levels, s scratch
+    DevArray<double> gdense;         // blocked Gauss-Seidel group blocks (A->st->blocked)
     int n = 0;
 };
 struct DevHierarchy {
@@ -110,7 +111,18 @@ struct WorkSys {
     DevArray<double> w; // scaling weights (nv + np)
     bool scaled = false;
 };
+struct StreamOwner {
+    cudaStream_t s = nullptr;
+    ~StreamOwner()
+    {
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    }
+};
 struct Ctx {
+    StreamOwner owner; // first member: destroyed after every stream-ordered array
     int device = 0;
     cudaStream_t stream = nullptr;
     std::string err;

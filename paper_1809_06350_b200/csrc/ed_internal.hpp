@@ -41,22 +41,36 @@ void after_launch(const char* what);
 int64_t launch_count();
 std::string& prof_tag(); // ED_PROFILE attribution tag (e.g. hierarchy/level)
 
+// Host milliseconds spent in cudaMalloc/cudaFree (diagnostics, ED_AMG_VERBOSE).
+double& alloc_ms();
+double now_ms_host();
+
+// Stream that device arrays allocated on this thread are ordered on (the
+// calling context's stream inside every C-ABI entry point; null outside:
+// plain synchronous cudaMalloc/cudaFree).  Stream-ordered allocations come
+// from the device's memory pool, which keeps freed memory for reuse, so the
+// per-Newton-step AMG rebuild does not pay cudaMalloc/cudaFree (or their
+// implicit device synchronisation) for every temporary.
+cudaStream_t& alloc_stream();
+
 // Owning device array (move-only).
 template <class T>
 struct DevArray {
     T* p = nullptr;
     size_t n = 0;
+    cudaStream_t as = nullptr; // allocation stream (null: synchronous allocation)
     DevArray() = default;
     explicit DevArray(size_t count) { alloc(count); }
     DevArray(const DevArray&) = delete;
     DevArray& operator=(const DevArray&) = delete;
-    DevArray(DevArray&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevArray(DevArray&& o) noexcept : p(o.p), n(o.n), as(o.as) { o.p = nullptr; o.n = 0; }
     DevArray& operator=(DevArray&& o) noexcept
     {
         if (this != &o) {
             release();
             p = o.p;
             n = o.n;
+            as = o.as;
             o.p = nullptr;
             o.n = 0;
         }
@@ -68,12 +82,21 @@ struct DevArray {
         if (count == n && p) return;
         release();
         if (count == 0) return;
-        ED_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+        const double t0 = now_ms_host();
+        as = alloc_stream();
+        if (as) ED_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), as));
+        else ED_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+        alloc_ms() += now_ms_host() - t0;
         n = count;
     }
     void release()
     {
-        if (p) cudaFree(p);
+        if (p) {
+            const double t0 = now_ms_host();
+            if (as) cudaFreeAsync(p, as);
+            else cudaFree(p);
+            alloc_ms() += now_ms_host() - t0;
+        }
         p = nullptr;
         n = 0;
     }
@@ -148,6 +171,20 @@ struct BsrStruct {
     int cluster = 0;             // > 0: cluster-resident sweep over this many CTAs (z in DSMEM)
     int avg_rows_per_level = 0;
     DevArray<int> d_lev_ptr;     // device copy of lev_ptr
+    // blocked sweep (narrow schedules whose z fits one CTA's shared memory):
+    // groups of 32/Rb consecutive stored rows; one warp solves a group's
+    // scalar rows in sweep order while the other warps sum the next group's
+    // rows over everything outside it (kernels_sparse.cu: k_sgs_blocked)
+    bool blocked = false;
+    int ngroups = 0;
+    DevArray<int> colp; // [nnzb] stored position of each block's column
+    DevArray<int> imap; // [ngroups][3][32*32] value index of the group's own / previous / next block, col-major, -1: 0
+    DevArray<int> gunit;  // [ngroups+1] first unit of each group
+    DevArray<int4> units; // (local row, k0, k1, first unit of the row) row-chunk units of the producers' sums
+    DevArray<int> rowu;   // [ngroups][33] first unit of each local row (relative to the group), last = count
+    int max_units = 0;    // per group
+    static constexpr int kBlockedMaxScalars = 20480;
+    static constexpr int kBlockedMaxUnits = 1024;
     // host mirrors
     std::vector<int> h_rowptr, h_col, h_perm, h_inv;
     int nlev() const { return static_cast<int>(lev_ptr.size()) - 1; }
@@ -201,8 +238,11 @@ void spmv(const Bsr& M, const double* x, double* y, const double* b, int mode, c
 void spmv2(const Bsr& M1, const double* x1, const Bsr& M2, const double* x2, double* y, double sgn,
            cudaStream_t s);
 // one in-place Gauss-Seidel half sweep over the level schedule (dataflow kernel)
+// dense: the operator's group blocks (blocked_dense) when A.st->blocked
 void sgs_sweep(const Bsr& A, const double* b, double* z, const double* inv_diag, bool forward,
-               cudaStream_t s);
+               cudaStream_t s, const double* dense = nullptr);
+// own / previous / next group blocks of a blocked-sweep operator (values as of the call)
+void blocked_dense(const Bsr& A, DevArray<double>& dense, cudaStream_t s);
 // Jacobi relaxation z += w * inv_diag * (b - t)
 void jacobi_update(double* z, const double* b, const double* t, const double* inv_diag, double w,
                    int64_t n, cudaStream_t s);

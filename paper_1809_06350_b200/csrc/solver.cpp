@@ -254,6 +254,7 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o)
                 d.A = &d.Aown;
             }
             d.invd = std::move(D.invd);
+            blocked_dense(*d.A, d.gdense, s);
             d.s.alloc(d.n);
             if (l > 0) {
                 d.r.alloc(d.n);
@@ -293,6 +294,7 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o)
             d.A = &d.Aown;
         }
         d.invd.upload(H.inv_diag, s);
+        blocked_dense(*d.A, d.gdense, s);
         d.s.alloc(d.n);
         if (l > 0) {
             d.r.alloc(d.n);
@@ -320,8 +322,8 @@ void DevHierarchy::smooth(Ctx& c, int l, const double* b, double* z, int sweeps)
         return;
     }
     for (int k = 0; k < sweeps; ++k) {
-        sgs_sweep(*d.A, b, z, d.invd.p, true, c.stream);
-        sgs_sweep(*d.A, b, z, d.invd.p, false, c.stream);
+        sgs_sweep(*d.A, b, z, d.invd.p, true, c.stream, d.gdense.p);
+        sgs_sweep(*d.A, b, z, d.invd.p, false, c.stream, d.gdense.p);
     }
 }
 
