@@ -222,6 +222,15 @@ int ed_timer(ed_ctx* ctx, int op, float* ms);
  * bytes per launch, for k = 0 coupled K x, 1 A-plane SpMV, 2 fine-level
  * Gauss-Seidel forward sweep on A, 3 S_hat SpMV. */
 int ed_bench_kernels(ed_ctx* ctx, const ed_block_solver_options* opts, int n_rep, double* out);
+/* Live kernel accounting: while on, every sparse launch (SpMV, Gauss-Seidel
+ * half sweep) is bracketed by CUDA events on its stream and attributed to
+ * "kernel@level" with its algorithmic bytes.  on = 1 clears the totals. */
+int ed_kernel_accounting(ed_ctx* ctx, int on);
+/* Number of accounted kernel classes (resolves pending events). */
+int ed_kernel_account_count(ed_ctx* ctx, int* n);
+/* Class idx: name, launches, total device ms, total algorithmic bytes. */
+int ed_kernel_account_get(ed_ctx* ctx, int idx, char* name, int name_cap, int64_t* launches, double* ms,
+                          double* bytes);
 
 #ifdef __cplusplus
 }

@@ -377,6 +377,22 @@ class Context:
         names = ("coupled_spmv", "a_spmv", "sgs_fwd_fine", "shat_spmv")
         return {k: (float(out[2 * i]), float(out[2 * i + 1])) for i, k in enumerate(names)}
 
+    def kernel_accounting(self, on: bool):
+        """Bracket every sparse launch with CUDA events (bench.py roofline)."""
+        self._chk(N.lib().ed_kernel_accounting(self._p, int(on)))
+
+    def kernel_account(self):
+        """{"kernel@level": (launches, total ms, total algorithmic bytes)} since accounting was switched on."""
+        n = C.c_int(0)
+        self._chk(N.lib().ed_kernel_account_count(self._p, C.byref(n)))
+        out = {}
+        for i in range(n.value):
+            name = C.create_string_buffer(128)
+            la, ms, by = N._i64(0), C.c_double(0.0), C.c_double(0.0)
+            self._chk(N.lib().ed_kernel_account_get(self._p, i, name, 128, C.byref(la), C.byref(ms), C.byref(by)))
+            out[name.value.decode()] = (int(la.value), float(ms.value), float(by.value))
+        return out
+
     @staticmethod
     def kernel_launches():
         return int(N.lib().ed_kernel_launches(None))

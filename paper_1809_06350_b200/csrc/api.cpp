@@ -56,6 +56,64 @@ void after_launch(const char* what)
 
 int64_t launch_count() { return g_launches.load(); }
 
+namespace {
+struct Acct {
+    bool on = false;
+    struct Rec {
+        std::string name;
+        double bytes;
+        cudaEvent_t a, b;
+    };
+    std::vector<cudaEvent_t> pool;
+    std::vector<Rec> open;
+    struct Tot {
+        int64_t n = 0;
+        double ms = 0.0, bytes = 0.0;
+    };
+    std::map<std::string, Tot> tot;
+    cudaEvent_t get()
+    {
+        if (pool.empty()) {
+            cudaEvent_t e;
+            ED_CUDA(cudaEventCreate(&e));
+            return e;
+        }
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+    // resolve recorded launches (their streams must be complete)
+    void flush()
+    {
+        for (auto& r : open) {
+            float ms = 0.0f;
+            if (cudaEventSynchronize(r.b) == cudaSuccess && cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+                Tot& t = tot[r.name];
+                t.n += 1;
+                t.ms += ms;
+                t.bytes += r.bytes;
+            }
+            pool.push_back(r.a);
+            pool.push_back(r.b);
+        }
+        open.clear();
+    }
+} g_acct;
+} // namespace
+
+bool acct_on() { return g_acct.on; }
+
+void acct_begin(cudaStream_t s, const char* name, double bytes)
+{
+    Acct::Rec r{prof_tag().empty() ? std::string(name) : std::string(name) + "@" + prof_tag(), bytes, g_acct.get(),
+                g_acct.get()};
+    ED_CUDA(cudaEventRecord(r.a, s));
+    g_acct.open.push_back(r);
+    if (g_acct.open.size() > 8192) g_acct.flush();
+}
+
+void acct_end(cudaStream_t s) { ED_CUDA(cudaEventRecord(g_acct.open.back().b, s)); }
+
 cudaStream_t& alloc_stream()
 {
     static thread_local cudaStream_t s = nullptr;
@@ -923,6 +981,47 @@ int ed_bench_kernels(ed_ctx* ctx, const ed_block_solver_options* opts, int n_rep
         out[7] = W.S.bytes_per_spmv();
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
+    });
+}
+
+} // extern "C"
+
+extern "C" {
+
+int ed_kernel_accounting(ed_ctx* ctx, int on)
+{
+    return guarded(ctx, [&](Ctx& c) {
+        c.sync();
+        g_acct.flush();
+        if (on) g_acct.tot.clear();
+        g_acct.on = on != 0;
+    });
+}
+
+int ed_kernel_account_count(ed_ctx* ctx, int* n)
+{
+    return guarded(ctx, [&](Ctx& c) {
+        check(n != nullptr, ED_INVALID_ARGUMENT, "null count");
+        c.sync();
+        g_acct.flush();
+        *n = static_cast<int>(g_acct.tot.size());
+    });
+}
+
+int ed_kernel_account_get(ed_ctx* ctx, int idx, char* name, int name_cap, int64_t* launches, double* ms,
+                          double* bytes)
+{
+    return guarded(ctx, [&](Ctx&) {
+        check(idx >= 0 && idx < static_cast<int>(g_acct.tot.size()), ED_INVALID_ARGUMENT, "index out of range");
+        auto it = g_acct.tot.begin();
+        std::advance(it, idx);
+        if (name && name_cap > 0) {
+            std::strncpy(name, it->first.c_str(), static_cast<size_t>(name_cap) - 1);
+            name[name_cap - 1] = '\0';
+        }
+        if (launches) *launches = it->second.n;
+        if (ms) *ms = it->second.ms;
+        if (bytes) *bytes = it->second.bytes;
     });
 }
 

@@ -48,14 +48,16 @@ void gs_level_order(const BlockPattern& pat, std::vector<int>& order, std::vecto
 bool pattern_symmetric(const BlockPattern& pat)
 {
     if (pat.nbr != pat.nbc) return false;
+    int bad = 0;
+#pragma omp parallel for schedule(dynamic, 256) reduction(| : bad)
     for (int i = 0; i < pat.nbr; ++i)
-        for (int64_t k = pat.rowptr[i]; k < pat.rowptr[i + 1]; ++k) {
+        for (int64_t k = pat.rowptr[i]; k < pat.rowptr[i + 1] && !bad; ++k) {
             const int j = pat.col[k];
             const auto b = pat.col.begin() + pat.rowptr[j];
             const auto e = pat.col.begin() + pat.rowptr[j + 1];
-            if (!std::binary_search(b, e, i)) return false;
+            if (!std::binary_search(b, e, i)) bad = 1;
         }
-    return true;
+    return bad == 0;
 }
 
 BsrLayout make_layout(const BlockPattern& pat, const std::vector<int>& row_order, const std::vector<int>& level_of_pos)

@@ -293,3 +293,23 @@ void reorth_apply(Reducer& R, double* w, const double* const* dV, const double* 
 void multi_axpy(double* x, const double* const* dV, const double* y, int k, int64_t n, cudaStream_t s);
 
 } // namespace edb
+
+namespace edb {
+// Live per-kernel accounting (bench.py's roofline): CUDA events around each
+// sparse launch on its stream, resolved after the caller synchronises.
+bool acct_on();
+void acct_begin(cudaStream_t s, const char* name, double bytes);
+void acct_end(cudaStream_t s);
+struct AcctScope {
+    cudaStream_t s;
+    bool on;
+    AcctScope(cudaStream_t st, const char* name, double bytes) : s(st), on(acct_on())
+    {
+        if (on) acct_begin(s, name, bytes);
+    }
+    ~AcctScope()
+    {
+        if (on) acct_end(s);
+    }
+};
+} // namespace edb

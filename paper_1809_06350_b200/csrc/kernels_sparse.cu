@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "ed_internal.hpp"
 
@@ -154,6 +156,13 @@ __device__ __forceinline__ unsigned int ld_relaxed(const unsigned int* p)
     return v;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ void red_release_add(unsigned int* p, unsigned int v)
 {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -209,17 +218,22 @@ __device__ __forceinline__ void finish_row(const BsrArgs& m, double* z, bool val
     double acc[B];
 #pragma unroll
     for (int r = 0; r < B; ++r) acc[r] = 0.0;
+    // all z gathers of the prefetched blocks in flight at once (branch-free),
+    // then the products of the blocks that count (off-diagonal, present)
+    double zv[PF][B];
 #pragma unroll
     for (int q = 0; q < PF; ++q) {
-        const int c = P.c[q];
-        if (c >= 0 && c != P.row) {
+        const int64_t cc = P.c[q] >= 0 ? P.c[q] : 0;
 #pragma unroll
-            for (int d = 0; d < B; ++d) {
-                const double zv = CG ? __ldcg(z + static_cast<int64_t>(c) * B + d) : z[static_cast<int64_t>(c) * B + d];
+        for (int d = 0; d < B; ++d) zv[q][d] = CG ? __ldcg(z + cc * B + d) : z[cc * B + d];
+    }
 #pragma unroll
-                for (int r = 0; r < B; ++r) acc[r] = fma(P.v[q][r * B + d], zv, acc[r]);
-            }
-        }
+    for (int q = 0; q < PF; ++q) {
+        const bool use = P.c[q] >= 0 && P.c[q] != P.row;
+#pragma unroll
+        for (int d = 0; d < B; ++d)
+#pragma unroll
+            for (int r = 0; r < B; ++r) acc[r] = use ? fma(P.v[q][r * B + d], zv[q][d], acc[r]) : acc[r];
     }
     for (int k = P.kb + PF * L; k < P.ke; k += L) {
         const int c = __ldg(m.col + k);
@@ -258,7 +272,8 @@ __global__ void __launch_bounds__(kThreads) k_sgs_flow(BsrArgs m, const double* 
                                                        const double* __restrict__ invd, int nitems, int nlev,
                                                        const int* __restrict__ item_row,
                                                        const int* __restrict__ item_level,
-                                                       const int* __restrict__ lev_items, unsigned int* sync)
+                                                       const int* __restrict__ lev_items, unsigned int* sync,
+                                                       unsigned long long* trace)
 {
     // enough blocks per lane prefetched that no column index is loaded after the wait
     constexpr int PF = (B == 3) ? 3 : 4;
@@ -274,6 +289,7 @@ __global__ void __launch_bounds__(kThreads) k_sgs_flow(BsrArgs m, const double* 
         __syncthreads();
         if (t >= nitems) return;
         const int item = FWD ? t : nitems - 1 - t;
+        if (trace && threadIdx.x == 0) trace[item * 3 + 0] = globaltimer();
         const int lev = item_level[item];
         const int s = item_row[item] + g;
         const bool valid = s < item_row[item + 1];
@@ -288,8 +304,10 @@ __global__ void __launch_bounds__(kThreads) k_sgs_flow(BsrArgs m, const double* 
             }
             __syncthreads();
         }
+        if (trace && threadIdx.x == 0) trace[item * 3 + 1] = globaltimer();
         finish_row<B, L, PF, FWD, true>(m, z, valid, lane, P);
         __syncthreads();
+        if (trace && threadIdx.x == 0) trace[item * 3 + 2] = globaltimer();
         if (threadIdx.x == 0) red_release_add(done + lev, 1u); // publishes the CTA's z writes (bar.sync + release)
     }
 }
@@ -396,16 +414,21 @@ __global__ void __launch_bounds__(kClT) k_sgs_cluster(BsrArgs m, const double* _
             double acc[B];
 #pragma unroll
             for (int r = 0; r < B; ++r) acc[r] = 0.0;
+            {
+                double zv[kPFB][B];
 #pragma unroll
-            for (int j = 0; j < kPFB; ++j) {
-                const int c = P.c[j];
-                if (c >= 0 && c != P.row) {
+                for (int j = 0; j < kPFB; ++j) {
+                    const int cc = P.c[j] >= 0 ? P.c[j] : 0;
 #pragma unroll
-                    for (int d = 0; d < B; ++d) {
-                        const double zv = *zptr(c * B + d);
+                    for (int d = 0; d < B; ++d) zv[j][d] = *zptr(cc * B + d);
+                }
 #pragma unroll
-                        for (int r = 0; r < B; ++r) acc[r] = fma(P.v[j][r * B + d], zv, acc[r]);
-                    }
+                for (int j = 0; j < kPFB; ++j) {
+                    const bool use = P.c[j] >= 0 && P.c[j] != P.row;
+#pragma unroll
+                    for (int d = 0; d < B; ++d)
+#pragma unroll
+                        for (int r = 0; r < B; ++r) acc[r] = use ? fma(P.v[j][r * B + d], zv[j][d], acc[r]) : acc[r];
                 }
             }
             for (int k = P.kb + kPFB * G; k < P.ke; k += G) {
@@ -908,15 +931,32 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
     }
     ED_CUDA(cudaMemsetAsync(S.sync.p, 0, S.sync.n * sizeof(unsigned int), s));
     const int grid = std::min(S.nitems, 148 * 2);
+    // ED_FLOW_TRACE=<nitems>: dump per-item timestamps of the first forward sweep with that many items
+    static const int trace_n = std::getenv("ED_FLOW_TRACE") ? std::atoi(std::getenv("ED_FLOW_TRACE")) : -1;
+    static bool traced = false;
+    unsigned long long* tr = nullptr;
+    if (!traced && fwd && nlev == trace_n) ED_CUDA(cudaMallocManaged(&tr, sizeof(unsigned long long) * 3 * S.nitems));
     ED_LANES(S.L, {
         if (fwd)
             k_sgs_flow<B, LL, true><<<grid, kThreads, 0, s>>>(a, b, z, invd, S.nitems, nlev, S.item_row.p,
-                                                             S.item_level.p, S.lev_items.p, S.sync.p);
+                                                             S.item_level.p, S.lev_items.p, S.sync.p, tr);
         else
             k_sgs_flow<B, LL, false><<<grid, kThreads, 0, s>>>(a, b, z, invd, S.nitems, nlev, S.item_row.p,
-                                                              S.item_level.p, S.lev_items.p, S.sync.p);
+                                                              S.item_level.p, S.lev_items.p, S.sync.p, tr);
     })
     after_launch("k_sgs_flow");
+    if (tr) {
+        traced = true;
+        ED_CUDA(cudaStreamSynchronize(s));
+        std::vector<int> il(S.nitems);
+        ED_CUDA(cudaMemcpy(il.data(), S.item_level.p, sizeof(int) * S.nitems, cudaMemcpyDeviceToHost));
+        FILE* f = std::fopen("gpurun_out/flow_trace.txt", "w");
+        if (f) {
+            for (int i = 0; i < S.nitems; ++i) std::fprintf(f, "%d %d %llu %llu %llu\n", i, il[i], tr[3 * i], tr[3 * i + 1], tr[3 * i + 2]);
+            std::fclose(f);
+        }
+        cudaFree(tr);
+    }
 }
 
 } // namespace
@@ -924,6 +964,7 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
 void spmv(const Bsr& M, const double* x, double* y, const double* b, int mode, cudaStream_t s)
 {
     const int RB = M.st->Rb, CB = M.st->Cb;
+    AcctScope acct(s, "k_spmv", M.bytes_per_spmv());
     if (RB == 1 && CB == 1) return launch_spmv<1, 1>(M, x, y, b, mode, s);
     if (RB == 3 && CB == 3) return launch_spmv<3, 3>(M, x, y, b, mode, s);
     if (RB == 3 && CB == 1) return launch_spmv<3, 1>(M, x, y, b, mode, s);
@@ -936,6 +977,7 @@ void spmv2(const Bsr& M1, const double* x1, const Bsr& M2, const double* x2, dou
     const int RB = M1.st->Rb, C1 = M1.st->Cb, C2 = M2.st->Cb;
     if (M2.st->Rb != RB || M2.st->nbr != M1.st->nbr || M2.st->h_perm != M1.st->h_perm)
         throw Error(ED_INVALID_ARGUMENT, "spmv2: row layouts differ");
+    AcctScope acct(s, "k_spmv2", M1.bytes_per_spmv() + M2.bytes_per_spmv() - 8.0 * M1.st->nbr * RB);
     if (RB == 3 && C1 == 3 && C2 == 1) return launch_spmv2<3, 3, 1>(M1, x1, M2, x2, y, sgn, s);
     if (RB == 1 && C1 == 3 && C2 == 1) return launch_spmv2<1, 3, 1>(M1, x1, M2, x2, y, sgn, s);
     if (RB == 1 && C1 == 1 && C2 == 3) return launch_spmv2<1, 1, 3>(M1, x1, M2, x2, y, sgn, s);
@@ -965,6 +1007,14 @@ void sgs_sweep(const Bsr& A, const double* b, double* z, const double* invd, boo
     const int B = A.st->Rb;
     if (A.st->Cb != B) throw Error(ED_INVALID_ARGUMENT, "sgs: non-square blocks");
     if (!A.st->leveled && A.st->nbr > 1) throw Error(ED_INVALID_ARGUMENT, "sgs: operator has no level schedule");
+    const BsrStruct& S = *A.st;
+    // algorithmic bytes of one half sweep: blocks + column indices once, row
+    // pointers, b and inv_diag read, z read and written
+    const double bytes = static_cast<double>(S.nnzb) * (8.0 * B * B + 4.0) + 4.0 * (S.nbr + 1) +
+                         4.0 * 8.0 * S.nbr * B;
+    const char* kname = S.blocked ? "k_sgs_blocked" : S.cluster > 0 ? "k_sgs_cluster" : S.chain ? "k_sgs_chain"
+                                                                                              : "k_sgs_flow";
+    AcctScope acct(s, kname, bytes);
     if (B == 1) return launch_sgs<1>(A, b, z, invd, forward, s, dense);
     if (B == 3) return launch_sgs<3>(A, b, z, invd, forward, s, dense);
     throw Error(ED_UNSUPPORTED, "sgs: unsupported block size");
