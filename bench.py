@@ -81,6 +81,9 @@ class Clocks:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        if os.environ.get("BENCH_NO_SMI"):
+            self.p = None
+            return
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={q}", "--format=csv,noheader,nounits",
                                        "-lms", "500"], stdout=self.f, stderr=subprocess.DEVNULL)
@@ -250,7 +253,8 @@ def run_ours(args, world, rank, local, dist):
     l0 = ctx.kernel_launches()
     prof = _profiler_range()
     prof(True)  # ncu --profile-from-start off captures exactly the timed steps
-    ctx.kernel_accounting(True)  # CUDA events around every sparse launch, on the library stream
+    acct_on = os.environ.get("BENCH_NO_ACCT") is None
+    ctx.kernel_accounting(acct_on)  # CUDA events around every sparse launch, on the library stream
     ctx.timer_start()
     phase = []
     for _ in range(args.steps):

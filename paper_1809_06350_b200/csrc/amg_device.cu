@@ -20,11 +20,12 @@ inline int g1(int64_t n) { return static_cast<int>(std::max<int64_t>(1, (n + kT 
 
 struct Timer {
     bool on = std::getenv("ED_AMG_VERBOSE") != nullptr;
+    bool nosync = on && std::atoi(std::getenv("ED_AMG_VERBOSE")) == 2; // host timestamps only
     std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
     void lap(cudaStream_t s, const char* what, int lvl, long a, long b)
     {
         if (!on) return;
-        cudaStreamSynchronize(s);
+        if (!nosync) cudaStreamSynchronize(s);
         const auto now = std::chrono::steady_clock::now();
         std::fprintf(stderr, "[amg-dev] L%d %-12s %9.3f s  %ld %ld\n", lvl, what,
                      std::chrono::duration<double>(now - t).count(), a, b);

@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 
 #include <omp.h>
 
@@ -105,14 +106,72 @@ bool acct_on() { return g_acct.on; }
 
 void acct_begin(cudaStream_t s, const char* name, double bytes)
 {
+    if (g_acct.open.size() >= 8192) g_acct.flush(); // before the push: acct_end pairs with open.back()
     Acct::Rec r{prof_tag().empty() ? std::string(name) : std::string(name) + "@" + prof_tag(), bytes, g_acct.get(),
                 g_acct.get()};
     ED_CUDA(cudaEventRecord(r.a, s));
     g_acct.open.push_back(r);
-    if (g_acct.open.size() > 8192) g_acct.flush();
 }
 
-void acct_end(cudaStream_t s) { ED_CUDA(cudaEventRecord(g_acct.open.back().b, s)); }
+void acct_end(cudaStream_t s)
+{
+    if (!g_acct.open.empty()) ED_CUDA(cudaEventRecord(g_acct.open.back().b, s));
+}
+
+namespace {
+struct Cache {
+    std::mutex mu;
+    std::map<std::pair<cudaStream_t, size_t>, std::vector<void*>> free;
+    static size_t size_class(size_t bytes)
+    {
+        if (bytes <= 4096) return 4096;
+        int e = 63 - __builtin_clzll(bytes); // 2^e <= bytes < 2^(e+1)
+        const size_t step = size_t(1) << (e - 3);
+        return (bytes + step - 1) / step * step;
+    }
+} g_cache;
+} // namespace
+
+void* cache_alloc(size_t bytes, cudaStream_t s)
+{
+    const size_t c = Cache::size_class(bytes);
+    {
+        std::lock_guard<std::mutex> lk(g_cache.mu);
+        auto it = g_cache.free.find({s, c});
+        if (it != g_cache.free.end() && !it->second.empty()) {
+            void* p = it->second.back();
+            it->second.pop_back();
+            return p; // stream order makes the reuse safe: earlier uses precede later ones
+        }
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, c) != cudaSuccess) {
+        cudaGetLastError();
+        cache_release_stream(s); // give cached blocks back and retry once
+        ED_CUDA(cudaMalloc(&p, c));
+    }
+    return p;
+}
+
+void cache_free(void* p, size_t bytes, cudaStream_t s)
+{
+    std::lock_guard<std::mutex> lk(g_cache.mu);
+    g_cache.free[{s, Cache::size_class(bytes)}].push_back(p);
+}
+
+void cache_release_stream(cudaStream_t s)
+{
+    cudaStreamSynchronize(s);
+    std::lock_guard<std::mutex> lk(g_cache.mu);
+    for (auto it = g_cache.free.begin(); it != g_cache.free.end();) {
+        if (it->first.first == s) {
+            for (void* p : it->second) cudaFree(p);
+            it = g_cache.free.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
 
 cudaStream_t& alloc_stream()
 {

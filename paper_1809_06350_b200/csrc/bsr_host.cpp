@@ -192,7 +192,7 @@ std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLay
         S.colp.upload(colp, s);
         S.imap.upload(imap, s);
         // producer units: (row, chunk of <= 32*U blocks), U blocks per lane in flight
-        int chunk = 32 * (Rb == 3 ? 4 : 8);
+        int chunk = 32 * (Rb == 3 ? 2 : 8); // kernels_blocked.cu: kU3 / kU1 blocks per lane
         for (;;) {
             int worst = 0;
             for (int g = 0; g < ng; ++g) {

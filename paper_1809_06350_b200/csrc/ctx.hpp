@@ -117,6 +117,7 @@ struct StreamOwner {
     {
         if (s) {
             cudaStreamSynchronize(s);
+            cache_release_stream(s);
             cudaStreamDestroy(s);
         }
     }

@@ -52,6 +52,11 @@ double now_ms_host();
 // per-Newton-step AMG rebuild does not pay cudaMalloc/cudaFree (or their
 // implicit device synchronisation) for every temporary.
 cudaStream_t& alloc_stream();
+// stream-ordered caching allocator (api.cpp): size classes with <= 12.5%
+// slack, per-stream free lists; a cache miss is a plain cudaMalloc
+void* cache_alloc(size_t bytes, cudaStream_t s);
+void cache_free(void* p, size_t bytes, cudaStream_t s);
+void cache_release_stream(cudaStream_t s);
 
 // Owning device array (move-only).
 template <class T>
@@ -84,7 +89,7 @@ struct DevArray {
         if (count == 0) return;
         const double t0 = now_ms_host();
         as = alloc_stream();
-        if (as) ED_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), as));
+        if (as) p = static_cast<T*>(cache_alloc(count * sizeof(T), as));
         else ED_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
         alloc_ms() += now_ms_host() - t0;
         n = count;
@@ -93,7 +98,7 @@ struct DevArray {
     {
         if (p) {
             const double t0 = now_ms_host();
-            if (as) cudaFreeAsync(p, as);
+            if (as) cache_free(p, n * sizeof(T), as);
             else cudaFree(p);
             alloc_ms() += now_ms_host() - t0;
         }
@@ -243,6 +248,9 @@ void sgs_sweep(const Bsr& A, const double* b, double* z, const double* inv_diag,
                cudaStream_t s, const double* dense = nullptr);
 // own / previous / next group blocks of a blocked-sweep operator (values as of the call)
 void blocked_dense(const Bsr& A, DevArray<double>& dense, cudaStream_t s);
+// blocked half sweep (kernels_blocked.cu), A.st->blocked
+void sgs_blocked(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s,
+                 const double* dense);
 // Jacobi relaxation z += w * inv_diag * (b - t)
 void jacobi_update(double* z, const double* b, const double* t, const double* inv_diag, double w,
                    int64_t n, cudaStream_t s);

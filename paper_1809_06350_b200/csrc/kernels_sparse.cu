@@ -502,247 +502,6 @@ __global__ void __launch_bounds__(kClT) k_sgs_cluster(BsrArgs m, const double* _
 }
 
 
-// Blocked Gauss-Seidel half sweep for narrow, deep schedules (the dense
-// coarse operators of smoothed aggregation, ~1 row per dependency level).
-// Stored rows (a topological order of the sweep) are cut into groups of
-// GR = 32/B consecutive block rows, i.e. <= 32 scalar rows.  Sweeping group h:
-//   * warp 0 (solver) runs the scalar recurrence of the group in sweep order,
-//     one lane per scalar row: z_t = (b_t - acc_t) * invd_t, broadcast by
-//     shuffle, then every later row adds its coupling to z_t (the group's own
-//     dense block, staged in shared memory) -- and, in the same pass, the
-//     rows of the NEXT group add their coupling to z_t (the "fold" block);
-//   * warps 1..15 (producers) meanwhile stage the next group: its own and
-//     fold blocks, b and inv_diag, and its row sums over every column that is
-//     neither in the group being solved nor an earlier row of its own group.
-// One CTA barrier per group instead of one barrier per level; z lives in
-// shared memory in stored order.  The sums are the reference's row sums
-// (amg.cpp:311-322) split into partial sums in a different order (roundoff).
-constexpr int kBlkT = 512;
-constexpr int kBlkU3 = 4, kBlkU1 = 8; // blocks per lane in flight (B = 3 / 1)
-
-__device__ __forceinline__ void producers_sync() { asm volatile("bar.sync 1, 480;" ::: "memory"); }
-
-struct BlockedArgs {
-    const int* colp;
-    const double* dense; // [ng][3][32*32]: own / previous / next group block, col-major (c, t)
-    const int* gunit;
-    const int4* units;
-    const int* rowu;
-    int ng, nsc;
-};
-
-// One producer warp's unit: U blocks per lane, loaded before they are needed.
-template <int B, int U>
-struct UnitRegs {
-    int lr, kbeg, kend;
-    int sc[U];
-    double v[U][B * B];
-};
-
-template <int B, int U>
-__device__ __forceinline__ void unit_load(const BsrArgs& m, const BlockedArgs& q, int unit, int lane, UnitRegs<B, U>& R)
-{
-    const int4 rec = q.units[unit];
-    R.lr = rec.x;
-    R.kbeg = rec.y;
-    R.kend = rec.z;
-#pragma unroll
-    for (int j = 0; j < U; ++j) {
-        const int k = rec.y + j * 32 + lane;
-        const bool ok = k < rec.z;
-        R.sc[j] = ok ? q.colp[k] : -1;
-#pragma unroll
-        for (int e = 0; e < B * B; ++e) R.v[j][e] = ok ? m.val[static_cast<int64_t>(k) * (B * B) + e] : 0.0;
-    }
-}
-
-// Partial row sum of one unit over the columns outside `solving` and outside
-// the earlier rows of its own group `X` (those are the solver's).
-template <int B, int U, bool FWD>
-__device__ __forceinline__ void unit_sum(const UnitRegs<B, U>& R, const double* zs, int X, int solving, double* acc)
-{
-    constexpr int GR = 32 / B;
-#pragma unroll
-    for (int j = 0; j < U; ++j) {
-        const int c = R.sc[j];
-        if (c < 0) continue;
-        const int gc = c / GR;
-        if (gc == solving) continue;
-        if (gc == X) {
-            const int lc = c - X * GR;
-#pragma unroll
-            for (int d = 0; d < B; ++d) {
-                const double zv = zs[c * B + d];
-                const int cl = lc * B + d;
-#pragma unroll
-                for (int r = 0; r < B; ++r) {
-                    const int tl = R.lr * B + r;
-                    if (FWD ? cl > tl : cl < tl) acc[r] = fma(R.v[j][r * B + d], zv, acc[r]);
-                }
-            }
-        } else {
-#pragma unroll
-            for (int d = 0; d < B; ++d) {
-                const double zv = zs[c * B + d];
-#pragma unroll
-                for (int r = 0; r < B; ++r) acc[r] = fma(R.v[j][r * B + d], zv, acc[r]);
-            }
-        }
-    }
-}
-
-template <int B, bool FWD>
-__global__ void __launch_bounds__(kBlkT) k_sgs_blocked(BsrArgs m, BlockedArgs q, const double* __restrict__ bvec,
-                                                       double* z, const double* __restrict__ invd)
-{
-    constexpr int GR = 32 / B;
-    constexpr int U = B == 3 ? kBlkU3 : kBlkU1;
-    constexpr int NPW = 15; // producer warps
-    extern __shared__ double smem[];
-    const int nsc = q.nsc, ng = q.ng;
-    double* zs = smem;             // [nsc] stored order
-    double* Gs = zs + nsc;         // [2][32*32] own block, col-major (c, t)
-    double* Fs = Gs + 2048;        // [2][32*32] fold block
-    double* far = Fs + 2048;       // [2][32]
-    double* bs = far + 64;         // [2][32]
-    double* is = bs + 64;          // [2][32]
-    double* part = is + 64;        // [kBlockedMaxUnits][B]
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int nbr = m.nbr;
-    for (int i = tid; i < nsc; i += kBlkT) {
-        const int s = i / B, d = i - s * B;
-        zs[i] = z[static_cast<int64_t>(m.perm ? m.perm[s] : s) * B + d];
-    }
-    UnitRegs<B, U> P; // this producer warp's first unit of the next group, in flight across the barrier
-    auto prefetch = [&](int X) {
-        if (X < 0 || X >= ng) return;
-        const int u0 = q.gunit[X], nu = q.gunit[X + 1] - u0;
-        if (warp - 1 < nu) unit_load<B, U>(m, q, u0 + warp - 1, lane, P);
-    };
-    if (warp > 0) prefetch(FWD ? 0 : ng - 1);
-    __syncthreads();
-
-    // producers: stage group X into buffer `buf` while the solver works on `solving`
-    auto stage = [&](int X, int buf, int solving) {
-        const int ptid = tid - 32;
-        const int s0 = X * GR;
-        const int R = min(GR, nbr - s0);
-        const int Ts = R * B;
-        const int hf = FWD ? X + 1 : X - 1;
-        const double* dg = q.dense + static_cast<int64_t>(X) * 3 * 1024;
-        const double* df = (hf >= 0 && hf < ng) ? q.dense + (static_cast<int64_t>(hf) * 3 + (FWD ? 1 : 2)) * 1024 : nullptr;
-        double gv[3], fv[3];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            const int e = ptid + j * 480;
-            gv[j] = e < 1024 ? dg[e] : 0.0;
-            fv[j] = (e < 1024 && df) ? df[e] : 0.0;
-        }
-        double bb = 0.0, ii = 1.0;
-        int ru0 = 0, ru1 = 0;
-        if (ptid < Ts) {
-            const int s = s0 + ptid / B;
-            const int64_t gi = static_cast<int64_t>(m.perm ? m.perm[s] : s) * B + (ptid - (ptid / B) * B);
-            bb = bvec[gi];
-            ii = invd[gi];
-            ru0 = q.rowu[X * 33 + ptid / B];
-            ru1 = q.rowu[X * 33 + ptid / B + 1];
-        }
-        const int u0 = q.gunit[X], nu = q.gunit[X + 1] - u0;
-        for (int ul = warp - 1; ul < nu; ul += NPW) {
-            if (ul != warp - 1) unit_load<B, U>(m, q, u0 + ul, lane, P); // beyond the first: on demand
-            double acc[B];
-#pragma unroll
-            for (int r = 0; r < B; ++r) acc[r] = 0.0;
-            unit_sum<B, U, FWD>(P, zs, X, solving, acc);
-            for (int kb = P.kbeg + 32 * U; kb < P.kend; kb += 32 * U) { // long units reuse P
-                P.kbeg = kb;
-#pragma unroll
-                for (int j = 0; j < U; ++j) {
-                    const int k = kb + j * 32 + lane;
-                    const bool ok = k < P.kend;
-                    P.sc[j] = ok ? q.colp[k] : -1;
-#pragma unroll
-                    for (int e = 0; e < B * B; ++e) P.v[j][e] = ok ? m.val[static_cast<int64_t>(k) * (B * B) + e] : 0.0;
-                }
-                unit_sum<B, U, FWD>(P, zs, X, solving, acc);
-            }
-#pragma unroll
-            for (int r = 0; r < B; ++r) {
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
-            }
-            if (lane == 0)
-#pragma unroll
-                for (int r = 0; r < B; ++r) part[ul * B + r] = acc[r];
-        }
-        // the group staged next time: its first units go in flight now
-        prefetch(FWD ? X + 1 : X - 1);
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            const int e = ptid + j * 480;
-            if (e < 1024) {
-                Gs[buf * 1024 + e] = gv[j];
-                Fs[buf * 1024 + e] = fv[j];
-            }
-        }
-        if (ptid < 32) {
-            bs[buf * 32 + ptid] = bb;
-            is[buf * 32 + ptid] = ii;
-        }
-        producers_sync();
-        if (ptid < Ts) {
-            const int r = ptid - (ptid / B) * B;
-            double a = 0.0;
-            for (int u = ru0; u < ru1; ++u) a += part[u * B + r];
-            far[buf * 32 + ptid] = a;
-        }
-    };
-
-    if (warp > 0) stage(FWD ? 0 : ng - 1, 0, -1);
-    __syncthreads();
-    double carry = 0.0;
-    for (int it = 0; it < ng; ++it) {
-        const int h = FWD ? it : ng - 1 - it;
-        const int cb = it & 1;
-        if (warp == 0) {
-            const int R = min(GR, nbr - h * GR);
-            const int Ts = R * B;
-            const int t = lane;
-            double acc = t < Ts ? far[cb * 32 + t] + carry : 0.0;
-            const double bq = bs[cb * 32 + t], iq = is[cb * 32 + t];
-            const double* G = Gs + cb * 1024;
-            const double* F = Fs + cb * 1024;
-            double fold = 0.0, zval = 0.0;
-#pragma unroll 4
-            for (int j = 0; j < Ts; ++j) {
-                const int cur = FWD ? j : Ts - 1 - j;
-                const double g = G[cur * 32 + t], f = F[cur * 32 + t];
-                const double u = (bq - acc) * iq;
-                const double zj = __shfl_sync(0xffffffffu, u, cur);
-                if (t == cur) zval = u;
-                if (FWD ? t > cur : t < cur) acc = fma(g, zj, acc);
-                fold = fma(f, zj, fold);
-            }
-            if (t < Ts) zs[h * GR * B + t] = zval;
-            carry = fold;
-        } else if (it + 1 < ng) {
-            stage(FWD ? h + 1 : h - 1, cb ^ 1, h);
-        }
-        __syncthreads();
-    }
-    for (int i = tid; i < nsc; i += kBlkT) {
-        const int s = i / B, d = i - s * B;
-        z[static_cast<int64_t>(m.perm ? m.perm[s] : s) * B + d] = zs[i];
-    }
-}
-
-inline size_t blocked_smem_bytes(int nsc, int B)
-{
-    return (static_cast<size_t>(nsc) + 2048 + 2048 + 64 * 3 + static_cast<size_t>(BsrStruct::kBlockedMaxUnits) * B) *
-           sizeof(double);
-}
-
 // One Gauss-Seidel half sweep over narrow levels: a single CTA walks the
 // levels with a CTA barrier between them (no global atomics or polling).
 template <int B, int L, bool FWD>
@@ -873,20 +632,7 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
     const int nlev = S.nlev();
     const BsrArgs a = args_of(A);
     if (S.blocked) {
-        const int nsc = S.nbr * B;
-        const size_t smem = blocked_smem_bytes(nsc, B);
-        auto kern = fwd ? k_sgs_blocked<B, true> : k_sgs_blocked<B, false>;
-        static bool attr_done[2][2] = {};
-        bool& done = attr_done[B == 3][fwd ? 1 : 0];
-        if (!done) {
-            ED_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(blocked_smem_bytes(BsrStruct::kBlockedMaxScalars, B))));
-            done = true;
-        }
-        const BlockedArgs q{S.colp.p, dense, S.gunit.p, S.units.p, S.rowu.p, S.ngroups, nsc};
-        if (!dense) throw Error(ED_INVALID_ARGUMENT, "blocked Gauss-Seidel needs the operator's dense group blocks");
-        kern<<<1, kBlkT, smem, s>>>(a, q, b, z, invd);
-        after_launch("k_sgs_blocked");
+        sgs_blocked(A, b, z, invd, fwd, s, dense);
         return;
     }
     if (S.cluster > 0) {
@@ -983,22 +729,6 @@ void spmv2(const Bsr& M1, const double* x1, const Bsr& M2, const double* x2, dou
     if (RB == 1 && C1 == 1 && C2 == 3) return launch_spmv2<1, 1, 3>(M1, x1, M2, x2, y, sgn, s);
     if (RB == 1 && C1 == 1 && C2 == 1) return launch_spmv2<1, 1, 1>(M1, x1, M2, x2, y, sgn, s);
     throw Error(ED_UNSUPPORTED, "spmv2: unsupported block shape");
-}
-
-__global__ void k_blocked_dense(const int* __restrict__ imap, const double* __restrict__ val, double* dense, int64_t n)
-{
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < n) dense[i] = imap[i] >= 0 ? val[imap[i]] : 0.0;
-}
-
-void blocked_dense(const Bsr& A, DevArray<double>& dense, cudaStream_t s)
-{
-    const BsrStruct& S = *A.st;
-    if (!S.blocked) return;
-    const int64_t n = static_cast<int64_t>(S.ngroups) * 3 * 1024;
-    dense.alloc(n);
-    k_blocked_dense<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(S.imap.p, A.val.p, dense.p, n);
-    after_launch("k_blocked_dense");
 }
 
 void sgs_sweep(const Bsr& A, const double* b, double* z, const double* invd, bool forward, cudaStream_t s,
