@@ -45,6 +45,19 @@ struct DevSetupResult {
 // A0 given as a (possibly level-permuted) Bsr with block size == opts.block_size.
 DevSetupResult amg_build_device(const Bsr& A0, const AmgOpts& opts, cudaStream_t s);
 
+// One level of a collapsed coarse tail (dense_tail.cu): natural-order
+// operator, prolongator/restriction to the next level, inv_diag (device).
+struct DenseTailLevel {
+    const DBsr* A = nullptr;
+    const DBsr* P = nullptr;
+    const DBsr* R = nullptr;
+    const double* invd = nullptr;
+};
+// Row-major dense V-cycle operator of levels lv[0..] above a coarsest level
+// with the given row-major pseudo-inverse (n_c x n_c): out = V_{lv[0]}.
+void dense_vcycle_operator(const std::vector<DenseTailLevel>& lv, const std::vector<double>& pinv, int nc,
+                           int pre_sweeps, int post_sweeps, DevArray<double>& out, cudaStream_t s);
+
 // Helpers shared with the V-cycle construction.
 Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s);
 

@@ -919,7 +919,7 @@ int ed_amg_vcycle(ed_ctx* ctx, int which, const ed_block_solver_options* opts, c
         if (info) {
             info[0] = h.fallback ? 0 : h.n_levels();
             info[1] = h.fallback ? 1 : 0;
-            for (int l = 0; l < h.n_levels() && l < 16; ++l) info[2 + l] = h.lv[l].n;
+            for (int l = 0; l < h.n_levels() && l < 16; ++l) info[2 + l] = h.level_rows[l];
             if (h.fallback) info[2] = n;
         }
     });

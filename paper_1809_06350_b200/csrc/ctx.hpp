@@ -96,12 +96,17 @@ struct DevHierarchy {
     std::vector<DevLevel> lv;
     DevArray<double> pinv;
     int nc = 0;
+    // collapsed coarse tail (dense_tail.cu): the last entry of lv is level
+    // `tail`, whose whole sub-V-cycle is the dense row-major operator vtail
+    int tail = -1;
+    DevArray<double> vtail;
+    std::vector<int> level_rows; // scalar rows of every level of the full hierarchy
     double setup_host_ms = 0.0;
     void build(Ctx& c, const Bsr& A0, const AmgOpts& o);
     void vcycle(Ctx& c, const double* r, double* z);
     void cycle(Ctx& c, int l, const double* r, double* z);
     void smooth(Ctx& c, int l, const double* b, double* z, int sweeps);
-    int n_levels() const { return static_cast<int>(lv.size()); }
+    int n_levels() const { return static_cast<int>(level_rows.size()); }
 };
 
 // Working (scaled) copy of the system and everything solve_block_system builds.

@@ -227,6 +227,8 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o)
     cudaStream_t s = c.stream;
     opts = o;
     lv.clear();
+    level_rows.clear();
+    tail = -1;
     fallback = false;
     const double t0 = now_ms();
     const bool device_ok = o.block_size == A0.st->Rb && (A0.st->Rb == 1 || A0.st->Rb == 3) &&
@@ -242,11 +244,29 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o)
             return;
         }
         const int L = static_cast<int>(R.levels.size());
-        lv.resize(L);
-        for (int l = 0; l < L; ++l) {
+        level_rows.clear();
+        for (int l = 0; l < L; ++l) level_rows.push_back(R.levels[l].A.nbr * R.levels[l].A.Rb);
+        // collapse the coarse tail: the first level below the fine one small
+        // enough for a dense V-cycle operator (ED_DENSE_TAIL scalar rows, 0: off)
+        static const int tail_max = std::getenv("ED_DENSE_TAIL") ? std::atoi(std::getenv("ED_DENSE_TAIL")) : 4096;
+        tail = -1;
+        if (o.smoother == 1 && tail_max > 0)
+            for (int l = 1; l + 1 < L; ++l)
+                if (level_rows[l] <= tail_max) {
+                    tail = l;
+                    break;
+                }
+        const int La = tail >= 0 ? tail + 1 : L;
+        lv.resize(La);
+        for (int l = 0; l < La; ++l) {
             DevLevel& d = lv[l];
             DevLevelData& D = R.levels[l];
             d.n = D.A.nbr * D.A.Rb;
+            if (l == tail) {
+                d.r.alloc(d.n);
+                d.z.alloc(d.n);
+                break;
+            }
             if (l == 0) {
                 d.A = &A0;
             } else {
@@ -266,7 +286,14 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o)
             }
         }
         nc = R.nc;
-        pinv.upload(R.pinv, s);
+        if (tail >= 0) {
+            std::vector<DenseTailLevel> tl;
+            for (int l = tail; l + 1 < L; ++l)
+                tl.push_back(DenseTailLevel{&R.levels[l].A, &R.levels[l].P, &R.levels[l].R, R.levels[l].invd.p});
+            dense_vcycle_operator(tl, R.pinv, R.nc, o.pre_sweeps, o.post_sweeps, vtail, s);
+        } else {
+            pinv.upload(R.pinv, s);
+        }
         ED_CUDA(cudaStreamSynchronize(s));
         return;
     }
@@ -281,6 +308,9 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o)
     }
     const int L = static_cast<int>(hh.levels.size());
     const int Bc = (o.block_size == 3) ? 3 : 1;
+    tail = -1;
+    level_rows.clear();
+    for (int l = 0; l < L; ++l) level_rows.push_back(hh.levels[l].A.nrows);
     lv.resize(L);
     for (int l = 0; l < L; ++l) {
         DevLevel& d = lv[l];
@@ -334,8 +364,9 @@ void DevHierarchy::cycle(Ctx& c, int l, const double* r, double* z)
     cudaStream_t s = c.stream;
     const std::string saved = prof_tag();
     prof_tag() = (opts.block_size == 3 ? "A" : "S") + std::to_string(l);
-    if (l == n_levels() - 1) {
-        dense_gemv(pinv.p, r, z, nc, s); // COD min-norm solve (amg.cpp:331-334)
+    if (l == static_cast<int>(lv.size()) - 1) {
+        if (l == tail) dense_gemv(vtail.p, r, z, d.n, s); // collapsed coarse tail (dense_tail.cu)
+        else dense_gemv(pinv.p, r, z, nc, s);            // COD min-norm solve (amg.cpp:331-334)
         prof_tag() = saved;
         return;
     }
