@@ -760,7 +760,9 @@ Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s)
     std::vector<int> order, lvl;
     int nlev = 0;
     gs_level_order(pat, order, lvl, nlev);
-    const BsrLayout lay = make_layout(pat, order, lvl);
+    const int rcs = m.Rb == m.Cb ? ring_order(pat, m.Rb, order, lvl, nlev) : 0;
+    BsrLayout lay = make_layout(pat, order, lvl);
+    lay.ring_cs = rcs;
     out.st = bsr_make_struct(pat, lay, m.Rb, m.Cb, s);
     out.st->leveled = true;
     if (std::getenv("ED_AMG_VERBOSE"))

@@ -61,6 +61,7 @@ void cache_release_stream(cudaStream_t s);
 // Owning device array (move-only).
 template <class T>
 struct DevArray {
+    static constexpr size_t kPad = 256;
     T* p = nullptr;
     size_t n = 0;
     cudaStream_t as = nullptr; // allocation stream (null: synchronous allocation)
@@ -89,8 +90,10 @@ struct DevArray {
         if (count == 0) return;
         const double t0 = now_ms_host();
         as = alloc_stream();
-        if (as) p = static_cast<T*>(cache_alloc(count * sizeof(T), as));
-        else ED_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+        // kPad bytes of slack: 16-B-granular bulk (TMA) copies may round a
+        // range's end up past the last element (kernels_ring.cu)
+        if (as) p = static_cast<T*>(cache_alloc(count * sizeof(T) + kPad, as));
+        else ED_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T) + kPad));
         alloc_ms() += now_ms_host() - t0;
         n = count;
     }
@@ -98,7 +101,7 @@ struct DevArray {
     {
         if (p) {
             const double t0 = now_ms_host();
-            if (as) cache_free(p, n * sizeof(T), as);
+            if (as) cache_free(p, n * sizeof(T) + kPad, as);
             else cudaFree(p);
             alloc_ms() += now_ms_host() - t0;
         }
@@ -190,6 +193,23 @@ struct BsrStruct {
     int max_units = 0;    // per group
     static constexpr int kBlockedMaxScalars = 20480;
     static constexpr int kBlockedMaxUnits = 1024;
+    // cluster push sweep (kernels_ring.cu): rows of each level dealt to
+    // ring_cs CTAs, which own their z; CTA c computes, for every row of a
+    // level, the partial row sum over the columns it owns and pushes it to the
+    // row's owner (st.async + mbarrier); the matrix streams through a TMA-fed
+    // ring of per-(level, CTA) chunks
+    int ring_cs = 0;
+    int ring_slice = 0;     // max scalars of z owned by one CTA
+    int ring_cap = 0;       // ring bytes per CTA
+    int ring_part = 0;      // bytes of one partial-sum slot (kRingSlots slots, by level)
+    int64_t ring_npk = 0;   // packed off-diagonal blocks
+    int ring_maxm = 0;      // rows of the widest level (early-sum buffers)
+    DevArray<int4> rchunk;  // [nlev*cs][2] {seg0, rows of the level, pk0, pk1}, {s0, own rows, z offset, barrier flags}
+    DevArray<int4> rseg;    // [nlev*cs*rows] {pk0, pk1, owner << 24 | byte offset in its slot, na << 16 | nb}
+    DevArray<int> rpcol;    // [npk] local z index (scalars) of each packed block's column
+    DevArray<int> rpsrc;    // [npk] stored block index of each packed block
+    DevArray<int> rown;     // [nbr] original rows in (CTA, local) order
+    DevArray<int> rown_ptr; // [cs+1]
     // host mirrors
     std::vector<int> h_rowptr, h_col, h_perm, h_inv;
     int nlev() const { return static_cast<int>(lev_ptr.size()) - 1; }
@@ -213,6 +233,7 @@ struct Bsr {
 // Where each block of a pattern (block-CSR order) lands in the stored order.
 struct BsrLayout {
     std::vector<int> perm, inv, lev_ptr;
+    int ring_cs = 0; // > 0: rows of each level are dealt round-robin to ring_cs CTAs, CTA-major (ring_order)
     std::vector<int64_t> addr; // stored block index per pattern block
 };
 
@@ -228,6 +249,12 @@ std::vector<double> bsr_pack_values(const BsrStruct& st, const BsrLayout& lay, c
 // level[i] = 1 + max(level[j] : j < i, (i,j) in pattern).
 void gs_level_order(const BlockPattern& pat, std::vector<int>& order, std::vector<int>& level_of_pos,
                     int& nlev);
+// Cluster push sweep eligibility (kernels_ring.cu): when the operator's
+// vector slices fit a 16-CTA cluster's shared memory and every (level, CTA)
+// chunk fits the TMA ring, reorder the rows inside each level CTA-major
+// (round-robin deal) and return the cluster size; else 0 (order unchanged).
+int ring_order(const BlockPattern& pat, int B, std::vector<int>& order, const std::vector<int>& level_of_pos,
+               int nlev);
 bool pattern_symmetric(const BlockPattern& pat);
 Bsr bsr_from_csr(const HostCsr& a, int Rb, int Cb, bool leveled, cudaStream_t s);
 HostCsr bsr_to_csr(const Bsr& m, cudaStream_t s);
@@ -246,11 +273,23 @@ void spmv2(const Bsr& M1, const double* x1, const Bsr& M2, const double* x2, dou
 // dense: the operator's group blocks (blocked_dense) when A.st->blocked
 void sgs_sweep(const Bsr& A, const double* b, double* z, const double* inv_diag, bool forward,
                cudaStream_t s, const double* dense = nullptr);
-// own / previous / next group blocks of a blocked-sweep operator (values as of the call)
+// sweep auxiliary data (values as of the call): own / previous / next group
+// blocks of a blocked-sweep operator, packed blocks of a push-sweep operator
 void blocked_dense(const Bsr& A, DevArray<double>& dense, cudaStream_t s);
 // blocked half sweep (kernels_blocked.cu), A.st->blocked
 void sgs_blocked(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s,
                  const double* dense);
+// cluster push half sweep (kernels_ring.cu), A.st->ring_cs > 0; packed = ring_pack output
+void sgs_ring(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s,
+              const double* packed);
+// packed off-diagonal blocks + diagonal blocks in stored row order (values as of the call)
+void ring_pack(const Bsr& A, DevArray<double>& packed, cudaStream_t s);
+// push-sweep scratch: double-buffered early sums per segment of a level
+int push_scratch_bytes(int maxm, int B);
+// ring capacity (bytes per CTA) for own slices of `slice` scalars and `parts` bytes of partial slots
+int ring_capacity(int slice, int parts);
+// cluster size the ring sweep runs with on this device (16, 8; 0: unavailable)
+int ring_cluster_size();
 // Jacobi relaxation z += w * inv_diag * (b - t)
 void jacobi_update(double* z, const double* b, const double* t, const double* inv_diag, double w,
                    int64_t n, cudaStream_t s);

@@ -337,6 +337,7 @@ void launch(const Bsr& A, const double* b, double* z, const double* invd, bool f
 void blocked_dense(const Bsr& A, DevArray<double>& dense, cudaStream_t s)
 {
     const BsrStruct& S = *A.st;
+    if (S.ring_cs > 0) return ring_pack(A, dense, s); // push sweep: packed blocks (kernels_ring.cu)
     if (!S.blocked) return;
     const int64_t n = static_cast<int64_t>(S.ngroups) * 3 * 1024;
     const int64_t ntot = n + 1024;

@@ -299,3 +299,35 @@ def test_element_inversion_raises(oracle):
         ctx.assemble_residuals()
     with pytest.raises(api.ElementInversion):
         ctx.assemble_tangent(cp.ts)
+
+
+@pytest.mark.parametrize("n", [16, 20])
+def test_mid_cube_vcycle_and_newton_pass(oracle, n):
+    """Operators big enough for the cluster-ring sweep (>= 4096 block rows)
+    and a collapsed dense coarse tail: one V-cycle on A (1e-12 against the
+    reference's sequential sweeps) and a whole first Newton pass."""
+    cp = CubeProblem(n=n, nu=0.5)
+    P = _ref_problem(oracle, cp)
+    st = cp.seeded_state()
+    P.set_state(st.u, st.udot, st.p, st.pdot, st.v, st.vdot)
+    P.assemble_tangent()
+    planes = [P.tangent_plane(k) for k in range(4)]
+    ctx = api.Context(0)
+    ctx.set_block_system(*[_csr(m) for m in planes])
+    r = np.random.default_rng(11).uniform(-1, 1, cp.nv)
+    opts = cp.solver_options()
+    opts.amg_a = api.amg_options(3, 0)
+    zg, ig = ctx.amg_vcycle(r, 0, opts)
+    zr, ir = oracle.amg_vcycle_csr(planes[0], r, oracle.default_amg(3, 0))
+    assert ig["level_rows"] == ir["level_rows"], (ig, ir)
+    assert _rel(zg, zr) < 1e-12
+    ctx.close()
+    ctx = cp.context(0)
+    ctx.set_state(st)
+    opts = cp.solver_options()
+    out = ctx.newton_first_pass(cp.ts, opts)
+    ro = P.newton_first_pass(opts_to_ref(opts))
+    assert abs(out["norm"] - ro["norm"]) <= 1e-12 * ro["norm"]
+    _assert_stats(out["stats"], ro["stats"])
+    _assert_history(out["history"], ro["history"])
+    assert _rel(out["x"], ro["x"]) < X_TOL
