@@ -752,18 +752,32 @@ Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s)
     BlockPattern pat;
     pat.nbr = m.nbr;
     pat.nbc = m.nbc;
+    static const bool verbose = std::getenv("ED_AMG_VERBOSE") != nullptr;
+    double tl = now_ms_host();
+    auto lap = [&](const char* what) {
+        if (!verbose) return;
+        const double t = now_ms_host();
+        std::fprintf(stderr, "[level-op] %-14s %8.2f ms\n", what, t - tl);
+        tl = t;
+    };
     const std::vector<int> rp = m.rowptr.to_host(s);
     pat.rowptr.assign(rp.begin(), rp.end());
     pat.col = m.col.to_host(s);
     pat.col.resize(m.nnzb);
+    lap("download");
     if (!pattern_symmetric(pat)) throw Error(ED_UNSUPPORTED, "Gauss-Seidel operator pattern is not symmetric");
+    lap("symmetric");
     std::vector<int> order, lvl;
     int nlev = 0;
     gs_level_order(pat, order, lvl, nlev);
+    lap("levels");
     const int rcs = m.Rb == m.Cb ? ring_order(pat, m.Rb, order, lvl, nlev) : 0;
+    lap("ring order");
     BsrLayout lay = make_layout(pat, order, lvl);
     lay.ring_cs = rcs;
+    lap("layout");
     out.st = bsr_make_struct(pat, lay, m.Rb, m.Cb, s);
+    lap("struct");
     out.st->leveled = true;
     if (std::getenv("ED_AMG_VERBOSE"))
         std::fprintf(stderr,

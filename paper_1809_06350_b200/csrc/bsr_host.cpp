@@ -190,45 +190,72 @@ static void ring_build(BsrStruct& S, const BsrLayout& lay, cudaStream_t s)
         }
     }
     std::vector<int> rown, psrc, pcol, lev_of(n);
+    // (pk indices fit int32: checked below)
     for (int l = 0; l < nlev; ++l)
         for (int q = S.lev_ptr[l]; q < S.lev_ptr[l + 1]; ++q) lev_of[q] = l;
     for (int c = 0; c < cs; ++c) {
         own_ptr[c + 1] = own_ptr[c] + static_cast<int>(own[c].size());
         rown.insert(rown.end(), own[c].begin(), own[c].end());
     }
-    psrc.reserve(S.nnzb);
-    pcol.reserve(S.nnzb);
-    std::vector<int4> seg;
-    seg.reserve(static_cast<size_t>(n) * cs);
+    // packed blocks per level (off-diagonal), then every level in parallel:
+    // a counting sort of its blocks by (CTA owning the column, row, part) where
+    // part orders [columns on level l-1 | other levels | level l+1]: the first
+    // part is the forward sweep's late part, the last the backward's
+    std::vector<int64_t> lvl_pk(nlev + 1, 0);
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int l = 0; l < nlev; ++l) {
+        int64_t c0 = 0;
+        for (int q = S.lev_ptr[l]; q < S.lev_ptr[l + 1]; ++q)
+            for (int k = S.h_rowptr[q]; k < S.h_rowptr[q + 1]; ++k) c0 += lay.inv[S.h_col[k]] != q;
+        lvl_pk[l + 1] = c0;
+    }
+    for (int l = 0; l < nlev; ++l) lvl_pk[l + 1] += lvl_pk[l];
+    if (lvl_pk[nlev] >= (1LL << 31)) throw Error(ED_UNSUPPORTED, "push sweep: too many blocks");
+    psrc.resize(lvl_pk[nlev]);
+    pcol.resize(lvl_pk[nlev]);
+    std::vector<int4> seg(static_cast<size_t>(n) * cs);
+    bool too_long = false;
+#pragma omp parallel for schedule(dynamic, 8) reduction(|| : too_long)
     for (int l = 0; l < nlev; ++l) {
         const int a = S.lev_ptr[l], m = S.lev_ptr[l + 1] - a;
-        for (int c = 0; c < cs; ++c) {
-            const int pk0 = static_cast<int>(psrc.size());
-            chunk[(static_cast<size_t>(l) * cs + c) * 2] = make_int4(static_cast<int>(seg.size()), m, pk0, 0);
-            for (int q = a; q < a + m; ++q) {
-                // [columns on level l-1 | other levels | level l+1]: the first
-                // part is the forward sweep's late part, the last the backward's
-                const int k0 = static_cast<int>(psrc.size());
-                int na = 0, nb = 0;
-                for (int pass = 0; pass < 3; ++pass)
-                    for (int k = S.h_rowptr[q]; k < S.h_rowptr[q + 1]; ++k) {
-                        const int sc = lay.inv[S.h_col[k]];
-                        if (sc == q || owner[sc] != c) continue;
-                        const int lc = lev_of[sc];
-                        const int part_of = lc == l - 1 ? 0 : lc == l + 1 ? 2 : 1;
-                        if (part_of != pass) continue;
-                        psrc.push_back(k);
-                        pcol.push_back(zl[sc]);
-                        na += pass == 0;
-                        nb += pass == 2;
-                    }
-                if (na > 0xFFFF || nb > 0xFFFF) throw Error(ED_UNSUPPORTED, "push sweep: row segment too long");
-                seg.push_back(make_int4(k0, static_cast<int>(psrc.size()), (owner[q] << 24) | ((qown[q] * cs + c) * PB * 8),
-                                        (na << 16) | nb));
+        const int K = cs * m * 3;
+        std::vector<int> start(K + 1, 0);
+        auto key = [&](int q, int k) {
+            const int sc = lay.inv[S.h_col[k]];
+            const int lc = lev_of[sc];
+            const int part_of = lc == l - 1 ? 0 : lc == l + 1 ? 2 : 1;
+            return (owner[sc] * m + (q - a)) * 3 + part_of;
+        };
+        for (int q = a; q < a + m; ++q)
+            for (int k = S.h_rowptr[q]; k < S.h_rowptr[q + 1]; ++k)
+                if (lay.inv[S.h_col[k]] != q) ++start[key(q, k) + 1];
+        for (int i = 0; i < K; ++i) start[i + 1] += start[i];
+        std::vector<int> pos(start.begin(), start.end() - 1);
+        const int64_t base = lvl_pk[l];
+        for (int q = a; q < a + m; ++q)
+            for (int k = S.h_rowptr[q]; k < S.h_rowptr[q + 1]; ++k) {
+                const int sc = lay.inv[S.h_col[k]];
+                if (sc == q) continue;
+                const int64_t at = base + pos[key(q, k)]++;
+                psrc[at] = k;
+                pcol[at] = zl[sc];
             }
-            chunk[(static_cast<size_t>(l) * cs + c) * 2].w = static_cast<int>(psrc.size());
+        for (int c = 0; c < cs; ++c) {
+            chunk[(static_cast<size_t>(l) * cs + c) * 2] =
+                make_int4(cs * a + c * m, m, static_cast<int>(base + start[c * m * 3]),
+                          static_cast<int>(base + start[(c + 1) * m * 3]));
+            for (int qi = 0; qi < m; ++qi) {
+                const int kk = (c * m + qi) * 3;
+                const int na = start[kk + 1] - start[kk], nb = start[kk + 3] - start[kk + 2];
+                too_long = too_long || na > 0xFFFF || nb > 0xFFFF;
+                const int q = a + qi;
+                seg[static_cast<size_t>(cs) * a + c * m + qi] =
+                    make_int4(static_cast<int>(base + start[kk]), static_cast<int>(base + start[kk + 3]),
+                              (owner[q] << 24) | ((qown[q] * cs + c) * PB * 8), (na << 16) | nb);
+            }
         }
     }
+    if (too_long) throw Error(ED_UNSUPPORTED, "push sweep: row segment too long");
     S.ring_cs = cs;
     S.ring_slice = *std::max_element(cnt.begin(), cnt.end()) * B;
     S.ring_part = mown * cs * PB * 8;

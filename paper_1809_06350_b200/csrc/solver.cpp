@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cmath>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "amg_device.hpp"
@@ -235,7 +236,14 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o)
                            std::getenv("ED_HOST_AMG") == nullptr;
     if (device_ok) {
         // GPU setup (amg_device.cu); the host only aggregates and orthonormalises
+        static const bool verbose = std::getenv("ED_AMG_VERBOSE") != nullptr;
+        auto lap = [&](const char* what) {
+            if (!verbose) return;
+            ED_CUDA(cudaStreamSynchronize(s));
+            std::fprintf(stderr, "[amg-build] %-22s %8.2f ms\n", what, now_ms() - t0);
+        };
         DevSetupResult R = amg_build_device(A0, o, s);
+        lap("device setup");
         setup_host_ms = 0.0;
         if (R.fallback) {
             fallback = true;
@@ -286,6 +294,7 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o)
             }
         }
         nc = R.nc;
+        lap("level operators");
         if (tail >= 0) {
             std::vector<DenseTailLevel> tl;
             for (int l = tail; l + 1 < L; ++l)
@@ -295,6 +304,7 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o)
             pinv.upload(R.pinv, s);
         }
         ED_CUDA(cudaStreamSynchronize(s));
+        lap("dense tail");
         return;
     }
     const HostCsr A0h = bsr_to_csr(A0, s);
