@@ -38,7 +38,7 @@ namespace {
 
 namespace cg = cooperative_groups;
 
-constexpr int kT = 256;             // 8 warps: 7 workers (partials), 1 owner warp (solves, producer)
+constexpr int kT = 512;             // 16 warps: 15 workers (partials), 1 owner warp (solves, producer)
 constexpr int kW = kT - 32;
 constexpr int kNMB = 32;            // chunks in flight (mbarrier ring)
 constexpr int kDynMax = 225 * 1024; // dynamic shared memory per CTA
@@ -54,6 +54,7 @@ struct PushArgs {
     const int* own_ptr;
     int nlev, cap, slice, part, maxm;
     long long* prof;
+    int exp; // ED_PUSH_EXP (profiling builds only): 1 skip early sums, 2 skip late blocks
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(kT, 1) k_sgs_push(PushArgs q, const double* __
     const int rank = static_cast<int>(cl.block_rank());
     const int cs = static_cast<int>(cl.num_blocks());
     const int nlev = q.nlev, cap = q.cap;
-    const bool producer = tid == kT - 32;
+    const bool producer = tid == kW - 32; // lane 0 of the last worker warp (off the owner warp's path)
 
     if (tid == 0) {
         for (int i = 0; i < kNMB; ++i) mbar_init(&mbar[i], 1);
@@ -174,8 +175,11 @@ __global__ void __launch_bounds__(kT, 1) k_sgs_push(PushArgs q, const double* __
             n2 = q.chunk[(lev * cs + rank) * 2 + 1];
         }
     };
-    auto issue_more = [&](int consumed) {
-        while (issued < nlev && issued - consumed < kNMB) {
+    // at most max_issue chunks per call: in steady state one chunk is freed per
+    // level, and the table entry of the next chunk (loaded one issue ahead)
+    // then has a whole level to arrive instead of stalling the producer
+    auto issue_more = [&](int consumed, int max_issue) {
+        for (int it = 0; it < max_issue && issued < nlev && issued - consumed < kNMB; ++it) {
             const int m = n1.y, pk0 = n1.z, pk1 = n1.w, s0 = n2.x, nown = n2.y;
             const int ca = pk0 & ~3, ce = (pk1 + 3) & ~3, va = pk0 & ~1, ve = (pk1 + 1) & ~1;
             const int da = s0 & ~1, de = (s0 + nown + 1) & ~1;
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(kT, 1) k_sgs_push(PushArgs q, const double* __
     };
     if (producer) {
         load_next();
-        issue_more(0);
+        issue_more(0, kNMB);
     }
     // every CTA's barriers initialised before anyone pushes
     cl_sync();
@@ -311,8 +315,10 @@ __global__ void __launch_bounds__(kT, 1) k_sgs_push(PushArgs q, const double* __
                 double acc[B];
 #pragma unroll
                 for (int r = 0; r < B; ++r) acc[r] = es[j * B + r];
-                if (FWD) seg_sum(cur, h.x, h.x + na, 1, acc);
-                else seg_sum(cur, h.y - nb, h.y, 1, acc);
+                if (!(PROF && (q.exp & 2))) {
+                    if (FWD) seg_sum(cur, h.x, h.x + na, 1, acc);
+                    else seg_sum(cur, h.y - nb, h.y, 1, acc);
+                }
                 const int owner = h.z >> 24;
                 const uint32_t dst = mapa(part_u32, owner) + static_cast<uint32_t>(par * q.part + (h.z & 0xFFFFFF));
                 const uint32_t bar = mapa(pbar_u32 + 8 * par, owner);
@@ -330,7 +336,8 @@ __global__ void __launch_bounds__(kT, 1) k_sgs_push(PushArgs q, const double* __
             // ---- workers: products of the next level while the partials travel
             if (tid < kW) {
                 nxt = open_chunk(li + 1);
-                early(nxt, esum + ((li + 1) & 1) * q.maxm * B);
+                if (prof) pt[5] += clock64() - t1;
+                if (!(PROF && (q.exp & 1))) early(nxt, esum + ((li + 1) & 1) * q.maxm * B);
             }
         }
         const long long t2 = prof ? clock64() : 0;
@@ -402,7 +409,7 @@ __global__ void __launch_bounds__(kT, 1) k_sgs_push(PushArgs q, const double* __
             if (tid == kW) tr[8] = w7[2];
         }
         __syncthreads(); // new z visible to every warp; chunk li consumed
-        if (producer) issue_more(li + 1);
+        if (producer) issue_more(li + 1, 1);
         cur = nxt;
         if (prof) {
             const long long t4 = clock64();
@@ -415,6 +422,7 @@ __global__ void __launch_bounds__(kT, 1) k_sgs_push(PushArgs q, const double* __
     if (prof) {
         pt[4] = clock64() - t_start;
         for (int k = 0; k < 5; ++k) q.prof[rank * 8 + k] = pt[k];
+        q.prof[rank * 8 + 7] = pt[5];
     }
     if (prof7) {
         q.prof[rank * 8 + 5] = w7[0];
@@ -463,7 +471,8 @@ void launch(const Bsr& A, const double* b, double* z, const double* invd, bool f
     const int slice = (S.ring_slice + 1) & ~1;
     const PushArgs q{S.rchunk.p, S.rseg.p,     S.rpcol.p, packed,     packed + ((S.ring_npk + 1) & ~1LL) * B * B,
                      S.rown.p,   S.rown_ptr.p, S.nlev(),  S.ring_cap, slice,
-                     S.ring_part, S.ring_maxm, prof_on ? prof : nullptr};
+                     S.ring_part, S.ring_maxm, prof_on ? prof : nullptr,
+                     std::getenv("ED_PUSH_EXP") ? std::atoi(std::getenv("ED_PUSH_EXP")) : 0};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(S.ring_cs, 1, 1);
     cfg.blockDim = dim3(kT, 1, 1);
@@ -485,8 +494,8 @@ void launch(const Bsr& A, const double* b, double* z, const double* invd, bool f
         if (nprint++ < 8) {
             std::fprintf(stderr, "[push] B=%d %s nlev=%d rows=%d cs=%d cap=%d |", B, fwd ? "fwd" : "bwd", S.nlev(), S.nbr,
                          S.ring_cs, S.ring_cap);
-            for (int k = 0; k < 7; ++k) std::fprintf(stderr, " %.0f", prof[k] / static_cast<double>(S.nlev()));
-            std::fprintf(stderr, " cyc/level (late+push early-next own-solve sync | total | w7: wait solve)\n");
+            for (int k = 0; k < 8; ++k) std::fprintf(stderr, " %.0f", prof[k] / static_cast<double>(S.nlev()));
+            std::fprintf(stderr, " cyc/level (late+push early-next own-solve sync | total | w7: wait solve | open-next)\n");
             if (nprint == 1)
                 for (int r = 0; r < 2; ++r)
                     for (int li = 0; li < 40; ++li) {
