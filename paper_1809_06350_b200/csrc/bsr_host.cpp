@@ -309,10 +309,14 @@ BsrLayout make_layout(const BlockPattern& pat, const std::vector<int>& row_order
     return L;
 }
 
-static int auto_lanes(double avg_blocks)
+// lanes per block row: about one block per lane for multi-entry blocks; for
+// scalar (1x1) operators ~4 entries per lane, so each lane keeps several
+// independent loads in flight and the last partial pass wastes fewer lanes
+static int auto_lanes(double avg_blocks, int entries)
 {
+    const double per_lane = entries == 1 ? 4.0 : 1.0;
     int L = 2;
-    while (L < 32 && L * 2 < avg_blocks) L *= 2;
+    while (L < 32 && L * 2 * per_lane < avg_blocks) L *= 2;
     return L;
 }
 
@@ -328,7 +332,7 @@ std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLay
     S.nbc = pat.nbc;
     S.nnzb = pat.nnzb();
     const int n = pat.nbr;
-    S.L = lanes > 0 ? lanes : auto_lanes(n > 0 ? static_cast<double>(S.nnzb) / n : 1.0);
+    S.L = lanes > 0 ? lanes : auto_lanes(n > 0 ? static_cast<double>(S.nnzb) / n : 1.0, Rb * Cb);
     S.h_rowptr.assign(n + 1, 0);
     S.h_col.assign(S.nnzb, 0);
     bool identity = true;
