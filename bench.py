@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--cpu-sample-n", type=int, default=None, help="cube size of the CPU sample (default: the workload)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (profiling runs)")
+    ap.add_argument("--spmv-n", type=int, default=160,
+                    help="cube size of the standalone SpMV leg (the metric's 160^3 BSR SpMV GB/s); 0 skips it")
+    ap.add_argument("--ref-budget-s", type=float, default=240.0,
+                    help="reference arm: wall budget of the timed steps; beyond it each step is a smaller cube")
     a = ap.parse_args()
     cfg = {0: (10, 0.4, 1e-3), 1: (40, 0.5, 1e-3), 2: (100, 0.45, 0.1), 4: (160, 0.5, 0.1)}[a.config]
     a.n = a.n or cfg[0]
@@ -170,16 +174,31 @@ def run_reference(args, world, rank, dist):
     if rank != 0:
         return
     n = args.cpu_sample_n
-    for _ in range(args.warmup):
-        cpu_reference_step(n, args.nu, args.dt)
+    # the reference has no warm-up effects (no JIT, no caches across solves):
+    # warm the process once on a tiny cube instead of W full samples
+    if args.warmup > 0:
+        cpu_reference_step(4, args.nu, args.dt)
+    # bounded: one full first pass on the workload cube is ~36 s single-threaded;
+    # when K of them would exceed the budget, each step is a smaller seeded cube
+    # and the rate is normalised per unknown to the workload (said in `sample`)
+    t1, _, _ = cpu_reference_step(n, args.nu, args.dt) if args.steps * 36.0 > args.ref_budget_s else (None, None, None)
+    n_s = n
+    if t1 is not None:
+        per_step = args.ref_budget_s / args.steps
+        while n_s > 8 and t1 * (n_s / n) ** 3 > per_step:
+            n_s -= 4
     times = []
     for _ in range(args.steps):
-        t, out, cp = cpu_reference_step(n, args.nu, args.dt)
+        t, out, cp = cpu_reference_step(n_s, args.nu, args.dt)
         times.append(t)
     tot = sum(times)
-    value = args.steps / tot
-    sample = (f"reference (oracle/_ref, 1 thread) first corrector pass on the {n}^3 cube ({cp.nv + cp.np} unknowns, "
-              f"seeded, nu={args.nu}, dt={args.dt})" + ("" if n == args.n else f"; bounded sample of the {args.n}^3 workload"))
+    from paper_1809_06350_b200 import CubeProblem
+    cw = CubeProblem(n=args.n, nu=args.nu, dt=args.dt)
+    scale = (cp.nv + cp.np) / (cw.nv + cw.np)  # solves/s of the sample -> of the workload, per unknown
+    value = args.steps / tot * scale
+    sample = (f"reference (oracle/_ref, 1 thread) first corrector pass on the {n_s}^3 cube ({cp.nv + cp.np} unknowns, "
+              f"seeded, nu={args.nu}, dt={args.dt})"
+              + ("" if n_s == args.n else f"; bounded sample of the {args.n}^3 workload, rate scaled by unknowns ({scale:.4f})"))
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
@@ -189,6 +208,32 @@ def run_reference(args, world, rank, dist):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def spmv_leg(n, device, peak):
+    """The metric's BSR SpMV GB/s at the 160^3 cube (configs[4] size, 16.6 M
+    unknowns, ~9 GB coupled matrix >> 126 MB L2): mesh + residual + tangent
+    assembly on the device, then the coupled / A-plane / S_hat SpMVs and the fine
+    Gauss-Seidel half sweep, each timed with CUDA events over 5 launches."""
+    import gc
+
+    from paper_1809_06350_b200 import CubeProblem
+
+    t0 = time.perf_counter()
+    cp = CubeProblem(n=n, nu=0.5, dt=0.1)
+    ctx = cp.context(device)
+    ctx.set_state(cp.seeded_state())
+    ctx.assemble_residuals()
+    ctx.assemble_tangent(cp.ts)
+    k = ctx.bench_kernels(cp.solver_options(), n_rep=5)
+    out = {"n": n, "unknowns": cp.nv + cp.np, "tets": cp.mesh.n_tets, "setup_s": round(time.perf_counter() - t0, 1)}
+    for name, (ms, by) in k.items():
+        gbs = by / (ms * 1e-3) / 1e9
+        out[name] = {"ms": ms, "bytes": by, "achieved_gbs": gbs, "frac": gbs / peak}
+    ctx.close()
+    del ctx, cp
+    gc.collect()
+    return out
 
 
 def _profiler_range():
@@ -313,6 +358,7 @@ def run_ours(args, world, rank, local, dist):
                "sample": f"reference (oracle/_ref, 1 thread) first corrector pass on the {args.cpu_sample_n}^3 cube "
                          f"({cpc.nv + cpc.np} unknowns) in {t_cpu:.2f} s"
                          + ("" if args.cpu_sample_n == args.n else f" (bounded sample of the {args.n}^3 workload)")}
+    spmv = spmv_leg(args.spmv_n, local, peak) if args.spmv_n > 0 else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -328,6 +374,7 @@ def run_ours(args, world, rank, local, dist):
                      "note": ("Gauss-Seidel half sweeps keep the reference's sequential semantics: their time is "
                               "dependency levels x per-level latency, not bytes (DESIGN.md §4)"),
                      "live_kernels": dict(list(live.items())[:10]), "standalone_kernels": micro},
+        "spmv_cfg4": spmv,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms": e2e_ms, "host_inputs": "pinned", "phase_ms_last": e2e_phase},

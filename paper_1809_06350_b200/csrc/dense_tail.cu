@@ -55,13 +55,15 @@ cublasHandle_t blas(cudaStream_t s)
     return h;
 }
 
-// natural-order BSR -> column-major dense (ld = rows); D must be zeroed
+// natural-order BSR -> column-major dense (ld = rows); D must be zeroed.
+// One warp per block row, lanes over its blocks.
 __global__ void k_densify(const int* __restrict__ rowptr, const int* __restrict__ col, const double* __restrict__ val,
                           int nbr, int Rb, int Cb, double* D, int64_t ld)
 {
-    const int br = blockIdx.x * blockDim.x + threadIdx.x;
+    const int br = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
     if (br >= nbr) return;
-    for (int k = rowptr[br]; k < rowptr[br + 1]; ++k) {
+    for (int k = rowptr[br] + lane; k < rowptr[br + 1]; k += 32) {
         const int c = col[k];
         for (int r = 0; r < Rb; ++r)
             for (int d = 0; d < Cb; ++d)
@@ -98,7 +100,8 @@ void densify(const DBsr& m, DevArray<double>& D, cudaStream_t s)
     D.alloc(static_cast<size_t>(rows) * cols);
     D.zero(s);
     if (m.nbr == 0) return;
-    k_densify<<<grid_of(m.nbr), 256, 0, s>>>(m.rowptr.p, m.col.p, m.val.p, m.nbr, m.Rb, m.Cb, D.p, rows);
+    k_densify<<<grid_of(static_cast<int64_t>(m.nbr) * 32), 256, 0, s>>>(m.rowptr.p, m.col.p, m.val.p, m.nbr, m.Rb, m.Cb,
+                                                                      D.p, rows);
     after_launch("k_densify");
 }
 
