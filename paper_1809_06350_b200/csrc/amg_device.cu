@@ -736,10 +736,7 @@ Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s)
         st->nbr = m.nbr;
         st->nbc = m.nbc;
         st->nnzb = m.nnzb;
-        int L = 2;
-        const double avg = m.nbr ? static_cast<double>(m.nnzb) / m.nbr : 1.0;
-        while (L < 32 && L * 2 < avg) L *= 2;
-        st->L = L;
+        st->L = auto_lanes(m.nbr ? static_cast<double>(m.nnzb) / m.nbr : 1.0, m.Rb * m.Cb);
         st->rowptr = std::move(m.rowptr);
         st->col = std::move(m.col);
         st->lev_ptr = {0, m.nbr};

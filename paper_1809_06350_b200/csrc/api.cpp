@@ -181,7 +181,7 @@ cudaStream_t& alloc_stream()
 
 double& alloc_ms()
 {
-    static double t = 0.0;
+    static thread_local double t = 0.0;
     return t;
 }
 
@@ -200,7 +200,9 @@ Ctx::Ctx(int dev) : device(dev)
 {
     ED_CUDA(cudaSetDevice(dev));
     ED_CUDA(cudaStreamCreateWithFlags(&owner.s, cudaStreamNonBlocking));
+    ED_CUDA(cudaStreamCreateWithFlags(&owner2.s, cudaStreamNonBlocking));
     stream = owner.s;
+    stream2 = owner2.s;
     // keep freed pool memory for the next Newton step's AMG rebuild
     cudaMemPool_t pool;
     ED_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));

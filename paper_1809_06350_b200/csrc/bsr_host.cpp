@@ -312,7 +312,7 @@ BsrLayout make_layout(const BlockPattern& pat, const std::vector<int>& row_order
 // lanes per block row: about one block per lane for multi-entry blocks; for
 // scalar (1x1) operators ~4 entries per lane, so each lane keeps several
 // independent loads in flight and the last partial pass wastes fewer lanes
-static int auto_lanes(double avg_blocks, int entries)
+int auto_lanes(double avg_blocks, int entries)
 {
     const double per_lane = entries == 1 ? 4.0 : 1.0;
     int L = 2;

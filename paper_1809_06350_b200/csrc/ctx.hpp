@@ -102,7 +102,8 @@ struct DevHierarchy {
     DevArray<double> vtail;
     std::vector<int> level_rows; // scalar rows of every level of the full hierarchy
     double setup_host_ms = 0.0;
-    void build(Ctx& c, const Bsr& A0, const AmgOpts& o);
+    // s: stream the build is ordered on (null: c.stream)
+    void build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s = nullptr);
     void vcycle(Ctx& c, const double* r, double* z);
     void cycle(Ctx& c, int l, const double* r, double* z);
     void smooth(Ctx& c, int l, const double* b, double* z, int sweeps);
@@ -128,9 +129,11 @@ struct StreamOwner {
     }
 };
 struct Ctx {
-    StreamOwner owner; // first member: destroyed after every stream-ordered array
+    StreamOwner owner;  // first members: destroyed after every stream-ordered array
+    StreamOwner owner2;
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t stream2 = nullptr; // the S_hat hierarchy is built on it, concurrently with A's
     std::string err;
     Reducer red;
     double* pinned = nullptr; // host staging for small D2H reads

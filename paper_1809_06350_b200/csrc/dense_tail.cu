@@ -42,8 +42,8 @@ namespace {
 
 cublasHandle_t blas(cudaStream_t s)
 {
-    static cublasHandle_t h = nullptr;
-    static int dev = -1;
+    static thread_local cublasHandle_t h = nullptr; // one handle per host thread (hierarchies build concurrently)
+    static thread_local int dev = -1;
     int d = 0;
     ED_CUDA(cudaGetDevice(&d));
     if (!h || d != dev) {

@@ -256,6 +256,8 @@ void gs_level_order(const BlockPattern& pat, std::vector<int>& order, std::vecto
 int ring_order(const BlockPattern& pat, int B, std::vector<int>& order, const std::vector<int>& level_of_pos,
                int nlev);
 bool pattern_symmetric(const BlockPattern& pat);
+// lanes per block row of the BSR kernels for an average row length (bsr_host.cpp)
+int auto_lanes(double avg_blocks, int entries);
 Bsr bsr_from_csr(const HostCsr& a, int Rb, int Cb, bool leveled, cudaStream_t s);
 HostCsr bsr_to_csr(const Bsr& m, cudaStream_t s);
 BlockPattern block_pattern_of_csr(const HostCsr& a, int Rb, int Cb);

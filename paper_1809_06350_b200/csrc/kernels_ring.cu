@@ -516,12 +516,9 @@ void launch(const Bsr& A, const double* b, double* z, const double* invd, bool f
 
 } // namespace
 
-int ring_cluster_size()
+static int ring_cluster_size_query()
 {
-    // largest cluster (16 non-portable, else 8) of full-shared-memory CTAs the device can co-schedule
-    static int cs = -1;
-    if (cs >= 0) return cs;
-    cs = 0;
+    int cs = 0;
     auto kern = k_sgs_push<3, true, false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynMax) != cudaSuccess ||
         cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
@@ -547,6 +544,13 @@ int ring_cluster_size()
         }
         cudaGetLastError();
     }
+    return cs;
+}
+
+int ring_cluster_size()
+{
+    // largest cluster (16 non-portable, else 8) of full-shared-memory CTAs the device can co-schedule
+    static const int cs = ring_cluster_size_query(); // thread-safe once
     return cs;
 }
 

@@ -6,6 +6,8 @@
 // (j+2 doubles) and runs the Givens rotations and the convergence test with
 // the reference's own scalar arithmetic.
 #include <algorithm>
+#include <exception>
+#include <thread>
 #include <chrono>
 #include <cmath>
 
@@ -223,9 +225,9 @@ SolveRes gmres_dev(Ctx& c, DOp& op, DPrec* M, const double* b, double* x, const 
 // ---------------------------------------------------------------------------
 // AMG
 
-void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o)
+void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t stream)
 {
-    cudaStream_t s = c.stream;
+    cudaStream_t s = stream ? stream : c.stream;
     opts = o;
     lv.clear();
     level_rows.clear();
@@ -569,9 +571,30 @@ Stats solve_block_system_dev(Ctx& c, const double* d_rhs, double* d_x, const ed_
     c.sync();
     const double t_shat = now_ms() - tp;
     tp = now_ms();
+    // the two hierarchies are independent (AmgHierarchy::build on A and on
+    // S_hat, precond.cpp:44-50): S_hat's is built on a second host thread and
+    // stream while A's is built here; the V-cycles run on c.stream after both
     DevHierarchy amg_a, amg_s;
-    amg_a.build(c, W.A, amg_opts_from(o.amg_a, c, true, W.nv));
-    amg_s.build(c, W.S, amg_opts_from(o.amg_s, c, false, W.np));
+    const AmgOpts oa = amg_opts_from(o.amg_a, c, true, W.nv), os = amg_opts_from(o.amg_s, c, false, W.np);
+    std::exception_ptr err_s;
+    std::thread th([&] {
+        try {
+            alloc_stream() = c.stream2;
+            ED_CUDA(cudaSetDevice(c.device));
+            amg_s.build(c, W.S, os, c.stream2);
+            ED_CUDA(cudaStreamSynchronize(c.stream2));
+        } catch (...) {
+            err_s = std::current_exception();
+        }
+    });
+    try {
+        amg_a.build(c, W.A, oa);
+    } catch (...) {
+        th.join();
+        throw;
+    }
+    th.join();
+    if (err_s) std::rethrow_exception(err_s);
     c.sync();
     const double t_amg = now_ms() - tp;
     tp = now_ms();
