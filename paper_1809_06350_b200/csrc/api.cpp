@@ -201,8 +201,12 @@ Ctx::Ctx(int dev) : device(dev)
     ED_CUDA(cudaSetDevice(dev));
     ED_CUDA(cudaStreamCreateWithFlags(&owner.s, cudaStreamNonBlocking));
     ED_CUDA(cudaStreamCreateWithFlags(&owner2.s, cudaStreamNonBlocking));
+    ED_CUDA(cudaStreamCreateWithFlags(&owner3.s, cudaStreamNonBlocking));
+    ED_CUDA(cudaStreamCreateWithFlags(&owner4.s, cudaStreamNonBlocking));
     stream = owner.s;
     stream2 = owner2.s;
+    stream3 = owner3.s;
+    stream4 = owner4.s;
     // keep freed pool memory for the next Newton step's AMG rebuild
     cudaMemPool_t pool;
     ED_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));

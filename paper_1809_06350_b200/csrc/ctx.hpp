@@ -130,10 +130,11 @@ struct StreamOwner {
 };
 struct Ctx {
     StreamOwner owner;  // first members: destroyed after every stream-ordered array
-    StreamOwner owner2;
+    StreamOwner owner2, owner3, owner4;
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t stream2 = nullptr; // the S_hat hierarchy is built on it, concurrently with A's
+    cudaStream_t stream3 = nullptr, stream4 = nullptr; // dense-tail builds of the A / S_hat hierarchies
     std::string err;
     Reducer red;
     double* pinned = nullptr; // host staging for small D2H reads

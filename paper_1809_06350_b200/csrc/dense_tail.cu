@@ -13,7 +13,7 @@
 // V_l is built bottom-up with the reference's recursion, on n x n matrix
 // right-hand sides (columns = unit residuals):
 //   Z  = 0
-//   pre sweeps:  Z = T_f^-1 (I - U Z);  Z = T_b^-1 (I - L Z)     (amg.cpp:311-322)
+//   pre sweeps:  Zf = T_f^-1 (I - U Z);  Z = T_b^-1 (I - L Zf)   (amg.cpp:311-322)
 //   Res = I - A Z;  Z += P V_{l+1} R Res                         (amg.cpp:341-349)
 //   post sweeps: as the pre sweeps                                 (amg.cpp:351)
 // where L/U are the strict triangles of A and T_f = D' + L, T_b = D' + U with
@@ -72,17 +72,21 @@ __global__ void k_densify(const int* __restrict__ rowptr, const int* __restrict_
     }
 }
 
-// T = A with diagonal D' = 1/inv_diag; Lo/Up = strict triangles of A (column-major n x n)
-__global__ void k_split(const double* __restrict__ A, const double* __restrict__ invd, double* T, double* Lo,
-                        double* Up, int n)
+// T = A with diagonal D' = 1/inv_diag; Up = strict upper triangle of A (column-major n x n)
+__global__ void k_split(const double* __restrict__ A, const double* __restrict__ invd, double* T, double* Up, int n)
 {
     const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= static_cast<int64_t>(n) * n) return;
     const int i = static_cast<int>(idx % n), j = static_cast<int>(idx / n);
     const double a = A[idx];
     T[idx] = i == j ? 1.0 / invd[i] : a;
-    Lo[idx] = i > j ? a : 0.0;
     Up[idx] = i < j ? a : 0.0;
+}
+
+__global__ void k_recip(const double* __restrict__ invd, double* d, int n)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) d[i] = 1.0 / invd[i];
 }
 
 __global__ void k_identity(double* M, int n)
@@ -128,32 +132,40 @@ void dense_vcycle_operator(const std::vector<DenseTailLevel>& lv, const std::vec
     for (int l = static_cast<int>(lv.size()) - 1; l >= 0; --l) {
         const DenseTailLevel& L = lv[l];
         const int n = L.A->nbr * L.A->Rb;
-        DevArray<double> A, T, Lo, Up, Z, M, Pd, Rd, Rc, Ec;
+        DevArray<double> A, T, Up, Z, M, Pd, Rd, Rc, Ec, UZ, Dp;
         densify(*L.A, A, s);
         T.alloc(static_cast<size_t>(n) * n);
-        Lo.alloc(T.n);
         Up.alloc(T.n);
-        k_split<<<grid_of(static_cast<int64_t>(n) * n), 256, 0, s>>>(A.p, L.invd, T.p, Lo.p, Up.p, n);
+        k_split<<<grid_of(static_cast<int64_t>(n) * n), 256, 0, s>>>(A.p, L.invd, T.p, Up.p, n);
         after_launch("k_split");
+        Dp.alloc(n);
+        k_recip<<<grid_of(n), 256, 0, s>>>(L.invd, Dp.p, n);
+        after_launch("k_recip");
         Z.alloc(T.n);
         Z.zero(s);
         bool zero_z = true;
-        // one symmetric sweep on the matrix iterate Z (right-hand side I)
+        // one symmetric sweep on the matrix iterate Z (right-hand side I).
+        // Identities used (T_f = D' + L, T_b = D' + U, T_f Zf = I - U Z):
+        //   backward rhs  I - L Zf = U Z + D' Zf  (= D' Zf when Z = 0)
+        // so a sweep costs one GEMM (U Z; none from zero) and two TRSMs.
         auto sweep = [&]() {
-            // forward: Z = T_f^-1 (I - U Z)
+            // UZ = U Z (zero when Z = 0)
+            if (!zero_z) {
+                UZ.alloc(T.n);
+                ED_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, Up.p, n, Z.p, n, &zero, UZ.p, n));
+            }
+            // forward: Zf = T_f^-1 (I - U Z)
             identity(M, n, s);
-            if (!zero_z)
-                ED_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &mone, Up.p, n, Z.p, n, &one, M.p, n));
+            if (!zero_z) ED_BLAS(cublasDgeam(h, CUBLAS_OP_N, CUBLAS_OP_N, n, n, &one, M.p, n, &mone, UZ.p, n, M.p, n));
             ED_BLAS(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n, n,
                                 &one, T.p, n, M.p, n));
-            std::swap(Z, M);
-            zero_z = false;
-            // backward: Z = T_b^-1 (I - L Z)
-            identity(M, n, s);
-            ED_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &mone, Lo.p, n, Z.p, n, &one, M.p, n));
+            // backward: Z = T_b^-1 (U Z + D' Zf)
+            Z.alloc(T.n);
+            ED_BLAS(cublasDdgmm(h, CUBLAS_SIDE_LEFT, n, n, M.p, n, Dp.p, 1, Z.p, n));
+            if (!zero_z) ED_BLAS(cublasDgeam(h, CUBLAS_OP_N, CUBLAS_OP_N, n, n, &one, Z.p, n, &one, UZ.p, n, Z.p, n));
             ED_BLAS(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n, n,
-                                &one, T.p, n, M.p, n));
-            std::swap(Z, M);
+                                &one, T.p, n, Z.p, n));
+            zero_z = false;
         };
         for (int k = 0; k < pre_sweeps; ++k) sweep();
         // coarse correction: Z += P Vc R (I - A Z)

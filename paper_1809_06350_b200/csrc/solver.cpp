@@ -267,6 +267,40 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
                     break;
                 }
         const int La = tail >= 0 ? tail + 1 : L;
+        // the dense tail (GPU, cuBLAS) is built on its own host thread and
+        // stream while this thread builds the level operators above it (host
+        // level schedules); it reads only levels >= tail
+        std::exception_ptr err_t;
+        std::thread tail_th;
+        cudaStream_t ts = s == c.stream ? c.stream3 : c.stream4;
+        if (tail >= 0) {
+            cudaEvent_t ready;
+            ED_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+            ED_CUDA(cudaEventRecord(ready, s));
+            ED_CUDA(cudaStreamWaitEvent(ts, ready, 0));
+            ED_CUDA(cudaEventDestroy(ready));
+            tail_th = std::thread([&, ts] {
+                try {
+                    alloc_stream() = ts;
+                    ED_CUDA(cudaSetDevice(c.device));
+                    std::vector<DenseTailLevel> tl;
+                    for (int l = tail; l + 1 < L; ++l)
+                        tl.push_back(DenseTailLevel{&R.levels[l].A, &R.levels[l].P, &R.levels[l].R,
+                                                    R.levels[l].invd.p});
+                    dense_vcycle_operator(tl, R.pinv, R.nc, o.pre_sweeps, o.post_sweeps, vtail, ts);
+                    ED_CUDA(cudaStreamSynchronize(ts));
+                } catch (...) {
+                    err_t = std::current_exception();
+                }
+            });
+        }
+        struct Joiner {
+            std::thread& t;
+            ~Joiner()
+            {
+                if (t.joinable()) t.join();
+            }
+        } joiner{tail_th};
         lv.resize(La);
         for (int l = 0; l < La; ++l) {
             DevLevel& d = lv[l];
@@ -297,14 +331,9 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
         }
         nc = R.nc;
         lap("level operators");
-        if (tail >= 0) {
-            std::vector<DenseTailLevel> tl;
-            for (int l = tail; l + 1 < L; ++l)
-                tl.push_back(DenseTailLevel{&R.levels[l].A, &R.levels[l].P, &R.levels[l].R, R.levels[l].invd.p});
-            dense_vcycle_operator(tl, R.pinv, R.nc, o.pre_sweeps, o.post_sweeps, vtail, s);
-        } else {
-            pinv.upload(R.pinv, s);
-        }
+        if (tail < 0) pinv.upload(R.pinv, s);
+        if (tail_th.joinable()) tail_th.join();
+        if (err_t) std::rethrow_exception(err_t);
         ED_CUDA(cudaStreamSynchronize(s));
         lap("dense tail");
         return;
