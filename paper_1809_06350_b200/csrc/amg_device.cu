@@ -506,6 +506,76 @@ DBsr natural_copy(const Bsr& A, cudaStream_t s)
     return N;
 }
 
+
+// ---- symbolic SpGEMM with a per-warp column bitmap in shared memory --------
+// Warp per block row of C: the lanes mark the columns of every B row the A
+// row touches (atomicOr into the warp's bitmap), then PASS 0 counts the set
+// bits of the touched word range, PASS 1 writes the columns in ascending
+// order (popcount prefix over the words).  The touched range is cleared for
+// the next row.  Same pattern as csr_matmul's sorted rows (csr.cpp:132-166).
+template <int PASS>
+__global__ void k_sym_bitmap(const int* __restrict__ arp, const int* __restrict__ acol, const int* __restrict__ brp,
+                             const int* __restrict__ bcol, int n, int words, int* cnt, const int* __restrict__ crp,
+                             int* ccol)
+{
+    extern __shared__ unsigned int bm_smem[];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned int* bm = bm_smem + static_cast<size_t>(wib) * words;
+    for (int i = lane; i < words; i += 32) bm[i] = 0u;
+    __syncwarp();
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int I = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; I < n; I += nw) {
+        int lo = words, hi = -1;
+        for (int k = arp[I]; k < arp[I + 1]; ++k) {
+            const int K = acol[k];
+            for (int kb = brp[K] + lane; kb < brp[K + 1]; kb += 32) {
+                const int c = bcol[kb];
+                atomicOr(&bm[c >> 5], 1u << (c & 31));
+                lo = min(lo, c >> 5);
+                hi = max(hi, c >> 5);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        __syncwarp();
+        if (PASS == 0) {
+            int c = 0;
+            for (int w = lo + lane; w <= hi; w += 32) {
+                c += __popc(bm[w]);
+                bm[w] = 0u;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            if (lane == 0) cnt[I] = c;
+        } else {
+            int out = crp[I];
+            for (int w0 = lo; w0 <= hi; w0 += 32) {
+                const int w = w0 + lane;
+                unsigned int bits = w <= hi ? bm[w] : 0u;
+                const int pc = __popc(bits);
+                int incl = pc;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                int at = out + incl - pc;
+                while (bits) {
+                    const int b = __ffs(bits) - 1;
+                    ccol[at++] = w * 32 + b;
+                    bits &= bits - 1;
+                }
+                if (w <= hi) bm[w] = 0u;
+                out += __shfl_sync(0xffffffffu, incl, 31);
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // symbolic + numeric C = A B
 DBsr spgemm(const DBsr& A, const DBsr& B, cudaStream_t s)
 {
@@ -516,82 +586,121 @@ DBsr spgemm(const DBsr& A, const DBsr& B, cudaStream_t s)
     C.Rb = A.Rb;
     C.Cb = B.Cb;
     const int n = A.nbr;
-    DevArray<int64_t> cnt(n);
-    k_cand_count<<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, B.rowptr.p, n, cnt.p);
-    after_launch("k_cand_count");
-    const std::vector<int64_t> hc = cnt.to_host(s);
-    cnt.release();
-    std::vector<int> ucnt_all(n, 0);
-    std::vector<DevArray<int>> chunk_cols;
-    std::vector<int64_t> chunk_tot;
-    const int64_t kChunk = 1LL << 28; // candidates per chunk (1 GiB of int keys)
-    int r0 = 0;
-    while (r0 < n) {
-        int r1 = r0;
-        int64_t tot = 0;
-        while (r1 < n && (r1 == r0 || tot + hc[r1] <= kChunk)) tot += hc[r1++];
-        if (tot >= (1LL << 31)) throw Error(ED_UNSUPPORTED, "spgemm: row candidates exceed int32");
-        const int nseg = r1 - r0;
-        std::vector<int> seg(nseg + 1, 0);
-        for (int i = 0; i < nseg; ++i) seg[i + 1] = seg[i] + static_cast<int>(hc[r0 + i]);
-        DevArray<int> dseg;
-        dseg.upload(seg, s);
-        DevArray<int> keys(std::max<int64_t>(tot, 1)), sorted(std::max<int64_t>(tot, 1));
-        const bool wide = tot > 256LL * nseg; // long rows: a warp per row
-        if (wide)
-            k_cand_fill_warp<<<g1(32LL * nseg), kT, 0, s>>>(A.rowptr.p, A.col.p, B.rowptr.p, B.col.p, r0, r1, dseg.p,
-                                                           keys.p);
-        else
-            k_cand_fill<<<g1(nseg), kT, 0, s>>>(A.rowptr.p, A.col.p, B.rowptr.p, B.col.p, r0, r1, dseg.p, keys.p);
-        after_launch("k_cand_fill");
-        size_t tb = 0;
-        cub::DeviceSegmentedSort::SortKeys(nullptr, tb, keys.p, sorted.p, static_cast<int>(tot), nseg, dseg.p,
-                                           dseg.p + 1, s);
-        DevArray<unsigned char> tmp(std::max<size_t>(tb, 1));
-        ED_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp.p, tb, keys.p, sorted.p, static_cast<int>(tot), nseg, dseg.p,
-                                                   dseg.p + 1, s));
-        after_launch("cub_segmented_sort");
-        keys.release();
-        DevArray<int> uc(nseg);
-        if (wide)
-            k_unique_count_warp<<<g1(32LL * nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, uc.p);
-        else
-            k_unique_count<<<g1(nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, uc.p);
-        after_launch("k_unique_count");
-        const std::vector<int> huc = uc.to_host(s);
-        std::vector<int> uoff;
-        exclusive_scan_host(huc, uoff);
-        DevArray<int> duoff;
-        duoff.upload(uoff, s);
-        DevArray<int> cols(std::max(uoff[nseg], 1));
-        if (wide)
-            k_unique_write_warp<<<g1(32LL * nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, duoff.p, cols.p);
-        else
-            k_unique_write<<<g1(nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, duoff.p, cols.p);
-        after_launch("k_unique_write");
-        for (int i = 0; i < nseg; ++i) ucnt_all[r0 + i] = huc[i];
-        chunk_tot.push_back(uoff[nseg]);
-        chunk_cols.push_back(std::move(cols));
+    const int words = (B.nbc + 31) / 32;
+    int64_t tot_cand = 0; // products a*b (numeric kernel choice)
+    static const bool no_bitmap = std::getenv("ED_SPGEMM_SORT") != nullptr;
+    if (!no_bitmap && n > 0 && static_cast<int64_t>(words) * 4 <= 96 * 1024) {
+        // symbolic via per-warp bitmaps: count, device scan, fill
+        const int wpb = std::max(1, std::min(8, static_cast<int>((96 * 1024) / (static_cast<int64_t>(words) * 4))));
+        const size_t smem = static_cast<size_t>(wpb) * words * 4;
+        static bool attr = false;
+        if (!attr) {
+            ED_CUDA(cudaFuncSetAttribute(k_sym_bitmap<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+            ED_CUDA(cudaFuncSetAttribute(k_sym_bitmap<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+            attr = true;
+        }
+        const int blocks = static_cast<int>(std::min<int64_t>((n + wpb - 1) / wpb, 148LL * 16));
+        DevArray<int> cnt(n + 1);
+        DevArray<int64_t> ccand(n), ctot(1);
+        k_sym_bitmap<0><<<blocks, 32 * wpb, smem, s>>>(A.rowptr.p, A.col.p, B.rowptr.p, B.col.p, n, words, cnt.p,
+                                                       nullptr, nullptr);
+        after_launch("k_sym_bitmap");
+        k_cand_count<<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, B.rowptr.p, n, ccand.p);
+        after_launch("k_cand_count");
+        C.rowptr.alloc(n + 1);
+        size_t tb = 0, tb2 = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, C.rowptr.p, n + 1, s);
+        cub::DeviceReduce::Sum(nullptr, tb2, ccand.p, ctot.p, n, s);
+        DevArray<unsigned char> tmp(std::max<size_t>(std::max(tb, tb2), 1));
+        ED_CUDA(cudaMemsetAsync(cnt.p + n, 0, sizeof(int), s));
+        ED_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, C.rowptr.p, n + 1, s));
+        int total = 0;
+        ED_CUDA(cudaMemcpyAsync(&total, C.rowptr.p + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+        ED_CUDA(cub::DeviceReduce::Sum(tmp.p, tb2, ccand.p, ctot.p, n, s));
+        ED_CUDA(cudaMemcpyAsync(&tot_cand, ctot.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         ED_CUDA(cudaStreamSynchronize(s));
-        r0 = r1;
-    }
-    std::vector<int> rp;
-    exclusive_scan_host(ucnt_all, rp);
-    C.nnzb = rp[n];
-    C.rowptr.upload(rp, s);
-    C.col.alloc(std::max<int64_t>(C.nnzb, 1));
-    int64_t o = 0;
-    for (size_t i = 0; i < chunk_cols.size(); ++i) {
-        if (chunk_tot[i])
-            ED_CUDA(cudaMemcpyAsync(C.col.p + o, chunk_cols[i].p, chunk_tot[i] * sizeof(int), cudaMemcpyDeviceToDevice, s));
-        o += chunk_tot[i];
+        C.nnzb = total;
+        C.col.alloc(std::max<int64_t>(C.nnzb, 1));
+        k_sym_bitmap<1><<<blocks, 32 * wpb, smem, s>>>(A.rowptr.p, A.col.p, B.rowptr.p, B.col.p, n, words, nullptr,
+                                                       C.rowptr.p, C.col.p);
+        after_launch("k_sym_bitmap");
+    } else {
+        DevArray<int64_t> cnt(n);
+        k_cand_count<<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, B.rowptr.p, n, cnt.p);
+        after_launch("k_cand_count");
+        const std::vector<int64_t> hc = cnt.to_host(s);
+        cnt.release();
+        for (const int64_t v : hc) tot_cand += v;
+        std::vector<int> ucnt_all(n, 0);
+        std::vector<DevArray<int>> chunk_cols;
+        std::vector<int64_t> chunk_tot;
+        const int64_t kChunk = 1LL << 28; // candidates per chunk (1 GiB of int keys)
+        int r0 = 0;
+        while (r0 < n) {
+            int r1 = r0;
+            int64_t tot = 0;
+            while (r1 < n && (r1 == r0 || tot + hc[r1] <= kChunk)) tot += hc[r1++];
+            if (tot >= (1LL << 31)) throw Error(ED_UNSUPPORTED, "spgemm: row candidates exceed int32");
+            const int nseg = r1 - r0;
+            std::vector<int> seg(nseg + 1, 0);
+            for (int i = 0; i < nseg; ++i) seg[i + 1] = seg[i] + static_cast<int>(hc[r0 + i]);
+            DevArray<int> dseg;
+            dseg.upload(seg, s);
+            DevArray<int> keys(std::max<int64_t>(tot, 1)), sorted(std::max<int64_t>(tot, 1));
+            const bool wide = tot > 256LL * nseg; // long rows: a warp per row
+            if (wide)
+                k_cand_fill_warp<<<g1(32LL * nseg), kT, 0, s>>>(A.rowptr.p, A.col.p, B.rowptr.p, B.col.p, r0, r1, dseg.p,
+                                                               keys.p);
+            else
+                k_cand_fill<<<g1(nseg), kT, 0, s>>>(A.rowptr.p, A.col.p, B.rowptr.p, B.col.p, r0, r1, dseg.p, keys.p);
+            after_launch("k_cand_fill");
+            size_t tb = 0;
+            cub::DeviceSegmentedSort::SortKeys(nullptr, tb, keys.p, sorted.p, static_cast<int>(tot), nseg, dseg.p,
+                                               dseg.p + 1, s);
+            DevArray<unsigned char> tmp(std::max<size_t>(tb, 1));
+            ED_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp.p, tb, keys.p, sorted.p, static_cast<int>(tot), nseg, dseg.p,
+                                                       dseg.p + 1, s));
+            after_launch("cub_segmented_sort");
+            keys.release();
+            DevArray<int> uc(nseg);
+            if (wide)
+                k_unique_count_warp<<<g1(32LL * nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, uc.p);
+            else
+                k_unique_count<<<g1(nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, uc.p);
+            after_launch("k_unique_count");
+            const std::vector<int> huc = uc.to_host(s);
+            std::vector<int> uoff;
+            exclusive_scan_host(huc, uoff);
+            DevArray<int> duoff;
+            duoff.upload(uoff, s);
+            DevArray<int> cols(std::max(uoff[nseg], 1));
+            if (wide)
+                k_unique_write_warp<<<g1(32LL * nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, duoff.p, cols.p);
+            else
+                k_unique_write<<<g1(nseg), kT, 0, s>>>(sorted.p, dseg.p, nseg, duoff.p, cols.p);
+            after_launch("k_unique_write");
+            for (int i = 0; i < nseg; ++i) ucnt_all[r0 + i] = huc[i];
+            chunk_tot.push_back(uoff[nseg]);
+            chunk_cols.push_back(std::move(cols));
+            ED_CUDA(cudaStreamSynchronize(s));
+            r0 = r1;
+        }
+        std::vector<int> rp;
+        exclusive_scan_host(ucnt_all, rp);
+        C.nnzb = rp[n];
+        C.rowptr.upload(rp, s);
+        C.col.alloc(std::max<int64_t>(C.nnzb, 1));
+        int64_t o = 0;
+        for (size_t i = 0; i < chunk_cols.size(); ++i) {
+            if (chunk_tot[i])
+                ED_CUDA(cudaMemcpyAsync(C.col.p + o, chunk_cols[i].p, chunk_tot[i] * sizeof(int), cudaMemcpyDeviceToDevice, s));
+            o += chunk_tot[i];
+        }
     }
     const int E = C.Rb * C.Cb;
     C.val.alloc(std::max<int64_t>(C.nnzb * E, 1));
     C.val.zero(s);
     const int64_t threads = static_cast<int64_t>(n) * A.Rb;
-    int64_t tot_cand = 0;
-    for (const int64_t v : hc) tot_cand += v;
     const bool wide_rows = tot_cand > 256LL * std::max(n, 1);
     if (A.Rb == 3 && A.Cb == 3 && B.Cb == 3) {
         if (wide_rows)
