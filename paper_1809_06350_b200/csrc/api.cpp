@@ -199,10 +199,15 @@ std::string& prof_tag()
 Ctx::Ctx(int dev) : device(dev)
 {
     ED_CUDA(cudaSetDevice(dev));
-    ED_CUDA(cudaStreamCreateWithFlags(&owner.s, cudaStreamNonBlocking));
-    ED_CUDA(cudaStreamCreateWithFlags(&owner2.s, cudaStreamNonBlocking));
-    ED_CUDA(cudaStreamCreateWithFlags(&owner3.s, cudaStreamNonBlocking));
-    ED_CUDA(cudaStreamCreateWithFlags(&owner4.s, cudaStreamNonBlocking));
+    // the library stream and the A-hierarchy tail stream carry the critical
+    // path of the concurrent hierarchy builds: highest priority; the S_hat
+    // build (shorter, overlapped) runs at the lowest
+    int lo_prio = 0, hi_prio = 0;
+    ED_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    ED_CUDA(cudaStreamCreateWithPriority(&owner.s, cudaStreamNonBlocking, hi_prio));
+    ED_CUDA(cudaStreamCreateWithPriority(&owner2.s, cudaStreamNonBlocking, lo_prio));
+    ED_CUDA(cudaStreamCreateWithPriority(&owner3.s, cudaStreamNonBlocking, hi_prio));
+    ED_CUDA(cudaStreamCreateWithPriority(&owner4.s, cudaStreamNonBlocking, lo_prio));
     stream = owner.s;
     stream2 = owner2.s;
     stream3 = owner3.s;

@@ -5,6 +5,8 @@
 // device; per Krylov iteration the host reads back the new Hessenberg column
 // (j+2 doubles) and runs the Givens rotations and the convergence test with
 // the reference's own scalar arithmetic.
+#include <omp.h>
+
 #include <algorithm>
 #include <exception>
 #include <thread>
@@ -606,23 +608,40 @@ Stats solve_block_system_dev(Ctx& c, const double* d_rhs, double* d_x, const ed_
     DevHierarchy amg_a, amg_s;
     const AmgOpts oa = amg_opts_from(o.amg_a, c, true, W.nv), os = amg_opts_from(o.amg_s, c, false, W.np);
     std::exception_ptr err_s;
-    std::thread th([&] {
+    double ms_s = 0.0, ms_a = 0.0;
+    static const bool serial = std::getenv("ED_SERIAL_SETUP") != nullptr;
+    auto build_s = [&] {
+        const cudaStream_t prev_as = alloc_stream();
+        const int prev_omp = omp_get_max_threads();
         try {
+            const double t = now_ms();
             alloc_stream() = c.stream2;
             ED_CUDA(cudaSetDevice(c.device));
+            if (!serial) omp_set_num_threads(std::max(1, omp_get_num_procs() / 4)); // leave the cores to A's build
             amg_s.build(c, W.S, os, c.stream2);
             ED_CUDA(cudaStreamSynchronize(c.stream2));
+            ms_s = now_ms() - t;
         } catch (...) {
             err_s = std::current_exception();
         }
-    });
+        alloc_stream() = prev_as;
+        omp_set_num_threads(prev_omp);
+    };
+    std::thread th;
+    if (!serial) th = std::thread(build_s);
     try {
+        const double t = now_ms();
         amg_a.build(c, W.A, oa);
+        ED_CUDA(cudaStreamSynchronize(c.stream));
+        ms_a = now_ms() - t;
     } catch (...) {
-        th.join();
+        if (th.joinable()) th.join();
         throw;
     }
-    th.join();
+    if (serial) build_s();
+    if (th.joinable()) th.join();
+    static const bool tell = std::getenv("ED_SETUP_TIMES") != nullptr;
+    if (tell) std::fprintf(stderr, "[setup] A %.1f ms  S %.1f ms\n", ms_a, ms_s);
     if (err_s) std::rethrow_exception(err_s);
     c.sync();
     const double t_amg = now_ms() - tp;
