@@ -469,6 +469,16 @@ int ed_mesh_upload(ed_ctx* ctx, int n_nodes, int n_tets, const int32_t* tets, co
     });
 }
 
+int ed_mesh_coords(ed_ctx* ctx, int n_nodes, const double* xyz)
+{
+    return guarded(ctx, [&](Ctx& c) {
+        check(xyz != nullptr && n_nodes > 0, ED_INVALID_ARGUMENT, "bad coordinates");
+        c.h_xyz.assign(xyz, xyz + 3LL * n_nodes);
+        c.have_dofs = false; // the velocity layout (sweep partition) is rebuilt with them
+        c.sys_from_mesh = false;
+    });
+}
+
 int ed_dofs_build(ed_ctx* ctx, const uint8_t* fixed, int32_t* nv, int32_t* np)
 {
     return guarded(ctx, [&](Ctx& c) {

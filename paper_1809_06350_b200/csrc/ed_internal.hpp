@@ -210,6 +210,20 @@ struct BsrStruct {
     DevArray<int> rpsrc;    // [npk] stored block index of each packed block
     DevArray<int> rown;     // [nbr] original rows in (CTA, local) order
     DevArray<int> rown_ptr; // [cs+1]
+    // tiled cluster sweep (kernels_tile.cu): rows owned by spatial tiles of a
+    // 16-CTA cluster, z of each tile in its CTA's shared memory
+    int tile_cs = 0;
+    int tile_slice = 0;      // max scalars of z owned by one CTA
+    int tile_cap = 0;        // ring bytes per CTA
+    DevArray<int4> tent;     // per-CTA sub-chunk entries {s0, s1, kb, ke}
+    DevArray<int> tent_ptr;  // [cs+1]
+    DevArray<int> tent_info; // local z index of the first row << 1 | last entry of its level
+    DevArray<int4> tent_bwd; // backward sweep: levels in reverse
+    DevArray<int> tent_info_bwd;
+    DevArray<int4> thdr;     // [nbr] {kb, ke, original row, diagonal block}
+    DevArray<int> tcolz;     // [nnzb] owner << 24 | byte offset of the column's z in the owner's slice
+    DevArray<int> town;      // [nbr] original rows in (CTA, local) order
+    DevArray<int> town_ptr;  // [cs+1]
     // host mirrors
     std::vector<int> h_rowptr, h_col, h_perm, h_inv;
     int nlev() const { return static_cast<int>(lev_ptr.size()) - 1; }
@@ -234,6 +248,8 @@ struct Bsr {
 struct BsrLayout {
     std::vector<int> perm, inv, lev_ptr;
     int ring_cs = 0; // > 0: rows of each level are dealt round-robin to ring_cs CTAs, CTA-major (ring_order)
+    int tile_cs = 0; // > 0: rows are owned by tile_cs spatial tiles, CTA-major inside each level (tile_order)
+    std::vector<int> tile_owner; // [nbr] tile of each original row
     std::vector<int64_t> addr; // stored block index per pattern block
 };
 
@@ -255,6 +271,14 @@ void gs_level_order(const BlockPattern& pat, std::vector<int>& order, std::vecto
 // (round-robin deal) and return the cluster size; else 0 (order unchanged).
 int ring_order(const BlockPattern& pat, int B, std::vector<int>& order, const std::vector<int>& level_of_pos,
                int nlev);
+// Tiled cluster sweep eligibility (kernels_tile.cu): with row coordinates
+// (3 per block row) and a vector that fits a 16-CTA cluster's shared memory,
+// partition the rows into spatial tiles (equal-count x/y bisection), reorder
+// each level CTA-major and return the cluster size (owner per row in `owner`).
+int tile_order(const BlockPattern& pat, int B, const std::vector<double>& xyz, std::vector<int>& order,
+               const std::vector<int>& level_of_pos, int nlev, std::vector<int>& owner);
+int tile_capacity(int slice);
+void sgs_tile(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s);
 bool pattern_symmetric(const BlockPattern& pat);
 // lanes per block row of the BSR kernels for an average row length (bsr_host.cpp)
 int auto_lanes(double avg_blocks, int entries);

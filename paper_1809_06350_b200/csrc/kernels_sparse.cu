@@ -631,6 +631,10 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
     if (S.nitems == 0) return;
     const int nlev = S.nlev();
     const BsrArgs a = args_of(A);
+    if (S.tile_cs > 0) {
+        sgs_tile(A, b, z, invd, fwd, s);
+        return;
+    }
     if (S.ring_cs > 0) {
         sgs_ring(A, b, z, invd, fwd, s, dense);
         return;
@@ -746,7 +750,7 @@ void sgs_sweep(const Bsr& A, const double* b, double* z, const double* invd, boo
     // pointers, b and inv_diag read, z read and written
     const double bytes = static_cast<double>(S.nnzb) * (8.0 * B * B + 4.0) + 4.0 * (S.nbr + 1) +
                          4.0 * 8.0 * S.nbr * B;
- const char* kname = S.ring_cs > 0 ? "k_sgs_push" : S.blocked ? "k_sgs_blocked" : S.cluster > 0 ? "k_sgs_cluster" : S.chain ? "k_sgs_chain"
+ const char* kname = S.tile_cs > 0 ? "k_sgs_tile" : S.ring_cs > 0 ? "k_sgs_push" : S.blocked ? "k_sgs_blocked" : S.cluster > 0 ? "k_sgs_cluster" : S.chain ? "k_sgs_chain"
                                                                                               : "k_sgs_flow";
     AcctScope acct(s, kname, bytes);
     if (B == 1) return launch_sgs<1>(A, b, z, invd, forward, s, dense);
