@@ -153,27 +153,24 @@ __global__ void k_invdiag(const int* __restrict__ rowptr, const int* __restrict_
     for (int r = 0; r < B; ++r) invd[static_cast<int64_t>(I) * B + r] = d[r] != 0.0 ? 1.0 / d[r] : 1.0;
 }
 
-// row-sequential y = A x (csr.cpp:11-18 order, no FMA)
+// row-sequential y = A x (csr.cpp:11-18 order, no FMA): one thread per
+// scalar row (the scalar CSR row of a block row walks its blocks in column
+// order, entries d = 0..CB-1 inside each block)
 template <int RB, int CB>
 __global__ void k_spmv_seq(const int* __restrict__ rowptr, const int* __restrict__ col, const double* __restrict__ val,
                            int n, const double* __restrict__ x, double* y)
 {
-    const int I = blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int I = static_cast<int>(t / RB), r = static_cast<int>(t % RB);
     if (I >= n) return;
-    double acc[RB];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) acc[r] = 0.0;
+    double acc = 0.0;
     for (int k = rowptr[I]; k < rowptr[I + 1]; ++k) {
         const int c = col[k];
-        const double* v = val + static_cast<int64_t>(k) * RB * CB;
+        const double* v = val + static_cast<int64_t>(k) * RB * CB + r * CB;
 #pragma unroll
-        for (int r = 0; r < RB; ++r)
-#pragma unroll
-            for (int d = 0; d < CB; ++d)
-                acc[r] = __dadd_rn(acc[r], __dmul_rn(v[r * CB + d], x[static_cast<int64_t>(c) * CB + d]));
+        for (int d = 0; d < CB; ++d) acc = __dadd_rn(acc, __dmul_rn(v[d], x[static_cast<int64_t>(c) * CB + d]));
     }
-#pragma unroll
-    for (int r = 0; r < RB; ++r) y[static_cast<int64_t>(I) * RB + r] = acc[r];
+    y[t] = acc;
 }
 
 __global__ void k_mul_vec(double* w, const double* __restrict__ s, int64_t n)
@@ -1009,7 +1006,7 @@ DevSetupResult amg_build_device(const Bsr& A0, const AmgOpts& opts, cudaStream_t
             double lambda = 1.0;
             bool zero = false;
             for (int it = 0; it < 10; ++it) {
-                if (Bs == 3) k_spmv_seq<3, 3><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, v.p, w.p);
+                if (Bs == 3) k_spmv_seq<3, 3><<<g1(3LL * n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, v.p, w.p);
                 else k_spmv_seq<1, 1><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, v.p, w.p);
                 k_mul_vec<<<g1(nrows), kT, 0, s>>>(w.p, L.invd.p, nrows);
                 after_launch("k_spmv_seq");

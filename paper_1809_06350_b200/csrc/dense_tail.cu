@@ -25,6 +25,9 @@
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include "amg_device.hpp"
@@ -40,15 +43,24 @@ namespace {
             throw ::edb::Error(ED_CUDA_ERROR, std::string(#call) + ": cublas status " + std::to_string(st_)); \
     } while (0)
 
+// One cuBLAS handle per stream, created once and kept (handles are not
+// thread-safe; the concurrent A / S_hat tail builds run on different streams).
 cublasHandle_t blas(cudaStream_t s)
 {
-    static thread_local cublasHandle_t h = nullptr; // one handle per host thread (hierarchies build concurrently)
-    static thread_local int dev = -1;
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, cublasHandle_t> handles;
     int d = 0;
     ED_CUDA(cudaGetDevice(&d));
-    if (!h || d != dev) {
-        ED_BLAS(cublasCreate(&h));
-        dev = d;
+    cublasHandle_t h = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = handles.find({d, s});
+        if (it == handles.end()) {
+            ED_BLAS(cublasCreate(&h));
+            handles[{d, s}] = h;
+        } else {
+            h = it->second;
+        }
     }
     ED_BLAS(cublasSetStream(h, s));
     ED_BLAS(cublasSetPointerMode(h, CUBLAS_POINTER_MODE_HOST));
