@@ -191,6 +191,31 @@ int ed_newton_first_pass(ed_ctx* ctx, const ed_time_scalars* ts, const ed_block_
                          double* x, double* out_norm, ed_linear_stats* stats, double* history,
                          int32_t history_cap, int32_t* history_len, ed_phase_times* times);
 
+/* NonlinearConfig (timeint.hpp:26-30). */
+typedef struct {
+    double tol_R, tol_A;
+    int32_t l_max, pad;
+} ed_nonlinear_config;
+
+/* StepStats (timeint.hpp:35-45) without the vectors (res_history is an
+ * out-array of the call); linear = the accumulated LinearStats. */
+typedef struct {
+    int32_t converged, newton_iters, n_res, pad;
+    double res0, res_final, t_assembly;
+} ed_step_stats;
+
+/* One generalized-alpha time step (step_generalized_alpha, timeint.cpp:40-180)
+ * from the uploaded state y_n, which becomes y_{n+1}: predictor, corrector
+ * passes with the admissibility guard (element inversion, non-finite or
+ * >4x-growing residual: halve the last update, up to 30 times), the Newton
+ * convergence test ||R|| <= max(tol_R ||R_0||, tol_A), tangent, fold-in,
+ * solve_block_system and the two-stage update -- all on the device, one
+ * scalar read-back per pass.  res_history gets ||R_(l)|| per pass (up to
+ * res_cap). */
+int ed_step_generalized_alpha(ed_ctx* ctx, const ed_time_scalars* ts, const ed_nonlinear_config* nl,
+                              const ed_block_solver_options* opts, ed_step_stats* out, ed_linear_stats* linear,
+                              double* res_history, int32_t res_cap);
+
 /* ---- debug / parity entry points ----------------------------------------- */
 /* y = K x (BlockMatrix::matvec, blocksystem.hpp:27-33) on the current system
  * (unscaled), host vectors of length nv+np. */

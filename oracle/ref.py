@@ -267,6 +267,18 @@ class RefProblem:
         return dict(x=x, rhs=rhs, norm=float(nrm[0]), stats=st.as_dict(),
                     history=hist[: int(hl[0])].copy(), times=times.copy())
 
+    def step(self, opts=None, tol_r=1e-8, tol_a=1e-6, l_max=20, t_n=0.0, res_cap=64):
+        """step_generalized_alpha (timeint.cpp:40-180) on the stored state."""
+        opts = opts or default_solver_options()
+        info, hist = np.zeros(3, np.int32), np.zeros(res_cap)
+        st, ta = LinearStats(), np.zeros(1)
+        rc = lib().orc_step(self.h, C.byref(opts), tol_r, tol_a, l_max, t_n, _ip(info), _dp(hist), res_cap,
+                            C.byref(st), _dp(ta))
+        if rc:
+            raise RuntimeError(_err())
+        return dict(converged=int(info[0]), newton_iters=int(info[1]), res_history=hist[: min(int(info[2]), res_cap)].copy(),
+                    linear=st.as_dict(), t_assembly=float(ta[0]))
+
 
 def gmres_csr(A: Csr, b, x0=None, cfg=(50, 500, 1e-6, 1e-50), flexible=False, precond=0,
               amg: AmgOptions | None = None, hist_cap=100000):

@@ -25,7 +25,7 @@ EXPORTED = [
     "ed_mesh_upload", "ed_mesh_coords", "ed_dofs_build", "ed_set_material", "ed_set_loads", "ed_state_upload",
     "ed_state_download", "ed_assemble_residuals", "ed_assemble_tangent", "ed_tangent_export",
     "ed_foldin_download", "ed_block_system_upload", "ed_solve_block_system",
-    "ed_solve_block_system_device", "ed_newton_first_pass", "ed_block_matvec", "ed_gmres_a",
+    "ed_solve_block_system_device", "ed_newton_first_pass", "ed_step_generalized_alpha", "ed_block_matvec", "ed_gmres_a",
     "ed_amg_vcycle", "ed_shat_export", "ed_block_matvec_device", "ed_spmv_bytes", "ed_state_save",
     "ed_state_restore", "ed_timer", "ed_bench_kernels", "ed_kernel_accounting", "ed_kernel_account_count",
     "ed_kernel_account_get",
@@ -81,6 +81,20 @@ class TimeScalars(C.Structure):
         return self.alpha_f * self.gamma * self.dt
 
 
+class NonlinearConfig(C.Structure):
+    """NonlinearConfig (timeint.hpp:26-30)."""
+    _fields_ = [("tol_R", _f64), ("tol_A", _f64), ("l_max", _i32), ("pad", _i32)]
+
+
+class StepStats(C.Structure):
+    """StepStats (timeint.hpp:35-45) without the vectors."""
+    _fields_ = [("converged", _i32), ("newton_iters", _i32), ("n_res", _i32), ("pad", _i32), ("res0", _f64),
+                ("res_final", _f64), ("t_assembly", _f64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad"}
+
+
 class PhaseTimes(C.Structure):
     _fields_ = [("residual_ms", _f64), ("tangent_ms", _f64), ("planes_ms", _f64), ("shat_ms", _f64),
                 ("amg_setup_ms", _f64), ("fgmres_ms", _f64), ("update_ms", _f64), ("total_ms", _f64),
@@ -128,6 +142,9 @@ def lib():
                                                    C.POINTER(LinearStats), dp, _i32, ip]),
         "ed_newton_first_pass": (C.c_int, [P, C.POINTER(TimeScalars), C.POINTER(BlockSolverOptions), dp, dp,
                                            C.POINTER(LinearStats), dp, _i32, ip, C.POINTER(PhaseTimes)]),
+        "ed_step_generalized_alpha": (C.c_int, [P, C.POINTER(TimeScalars), C.POINTER(NonlinearConfig),
+                                                C.POINTER(BlockSolverOptions), C.POINTER(StepStats),
+                                                C.POINTER(LinearStats), dp, _i32]),
         "ed_block_matvec": (C.c_int, [P, dp, dp]),
         "ed_gmres_a": (C.c_int, [P, dp, dp, C.POINTER(KrylovConfig), C.c_int, C.c_int,
                                  C.POINTER(AmgOptions), C.POINTER(SolveResult), dp, _i32, ip]),

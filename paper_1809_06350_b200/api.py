@@ -301,6 +301,20 @@ class Context:
                                                C.byref(st), N.dp(h), hist_cap, C.byref(hl), C.byref(pt)))
         return dict(x=x, norm=nrm.value, stats=st.as_dict(), history=h[: hl.value].copy(), times=pt.as_dict())
 
+    def step(self, ts: N.TimeScalars, opts: N.BlockSolverOptions | None = None, tol_r=1e-8, tol_a=1e-6, l_max=20,
+             res_cap=64):
+        """step_generalized_alpha (timeint.cpp:40-180): one time step from the
+        current state (which becomes y_{n+1}); StepStats + accumulated LinearStats."""
+        opts = opts or block_solver_options()
+        nl = N.NonlinearConfig(tol_r, tol_a, l_max, 0)
+        st, lin, h = N.StepStats(), N.LinearStats(), np.zeros(res_cap)
+        self._chk(N.lib().ed_step_generalized_alpha(self._p, C.byref(ts), C.byref(nl), C.byref(opts), C.byref(st),
+                                                    C.byref(lin), N.dp(h), res_cap))
+        out = st.as_dict()
+        out["res_history"] = h[: min(st.n_res, res_cap)].copy()
+        out["linear"] = lin.as_dict()
+        return out
+
     # ---- debug / parity --------------------------------------------------
     def block_matvec(self, x):
         y = np.zeros(self.nv + self.np)

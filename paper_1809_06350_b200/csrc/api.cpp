@@ -4,6 +4,7 @@
 #include <atomic>
 #include <climits>
 #include <cmath>
+#include <limits>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -792,6 +793,154 @@ int ed_newton_first_pass(ed_ctx* ctx, const ed_time_scalars* ts, const ed_block_
         if (times) *times = T;
         fill_stats(st, stats);
         copy_hist(hist, history, history_cap, history_len);
+    });
+}
+
+int ed_step_generalized_alpha(ed_ctx* ctx, const ed_time_scalars* ts, const ed_nonlinear_config* nl,
+                              const ed_block_solver_options* opts, ed_step_stats* out, ed_linear_stats* linear,
+                              double* res_history, int32_t res_cap)
+{
+    return guarded(ctx, [&](Ctx& c) {
+        check(ts != nullptr && nl != nullptr && opts != nullptr, ED_INVALID_ARGUMENT, "null argument");
+        check(c.have_dofs && c.have_mat, ED_NOT_READY, "problem not defined");
+        cudaStream_t s = c.stream;
+        const int N = c.n_nodes;
+        const int64_t n3 = 3LL * N;
+        const double chi = ts->alpha_f * ts->gamma * ts->dt;
+        const double gdt = ts->gamma * ts->dt;
+        const int64_t nvv = 3 * static_cast<int64_t>(c.nfree);
+        // y_n (converged state at t_n) and the iterate before the last update
+        auto keep = [&](DevArray<double>& dst, const DevArray<double>& src) { dst.copy_from(src, s); };
+        keep(c.y_u, c.u);
+        keep(c.y_udot, c.udot);
+        keep(c.y_p, c.p);
+        keep(c.y_pdot, c.pdot);
+        keep(c.y_v, c.v);
+        keep(c.y_vdot, c.vdot);
+        c.q_u.alloc(n3);
+        c.q_udot.alloc(n3);
+        c.q_p.alloc(N);
+        c.q_pdot.alloc(N);
+        c.q_v.alloc(n3);
+        c.q_vdot.alloc(n3);
+        NewtonArgs na{};
+        na.yn_u = c.y_u.p;
+        na.yn_udot = c.y_udot.p;
+        na.yn_p = c.y_p.p;
+        na.yn_pdot = c.y_pdot.p;
+        na.yn_v = c.y_v.p;
+        na.yn_vdot = c.y_vdot.p;
+        na.cur_u = c.u.p;
+        na.cur_udot = c.udot.p;
+        na.cur_p = c.p.p;
+        na.cur_pdot = c.pdot.p;
+        na.cur_v = c.v.p;
+        na.cur_vdot = c.vdot.p;
+        na.mid_u = c.m_u.p;
+        na.mid_udot = c.m_udot.p;
+        na.mid_p = c.m_p.p;
+        na.mid_pdot = c.m_pdot.p;
+        na.mid_v = c.m_v.p;
+        na.mid_vdot = c.m_vdot.p;
+        na.n_nodes = N;
+        na.pf = (ts->gamma - 1.0) / ts->gamma;
+        na.alpha_m = ts->alpha_m;
+        na.alpha_f = ts->alpha_f;
+        NewtonArgs nh = na; // halving: prev in the yn slots
+        nh.yn_u = c.q_u.p;
+        nh.yn_udot = c.q_udot.p;
+        nh.yn_p = c.q_p.p;
+        nh.yn_pdot = c.q_pdot.p;
+        nh.yn_v = c.q_v.p;
+        nh.yn_vdot = c.q_vdot.p;
+        // predictor + first stage blend (timeint.cpp:57-61, 88-93)
+        launch_predict_blend(na, s);
+        ed_step_stats st{};
+        Stats lin;
+        std::vector<double> hist;
+        constexpr double kGrowthCap = 4.0; // timeint.cpp:73
+        double norm_prev = std::numeric_limits<double>::infinity();
+        DevArray<double> nr(3);
+        bool first_blend = true;
+        for (int l = 1; l <= nl->l_max + 1; ++l) {
+            double norm = 0.0;
+            for (int halvings = 0;; ++halvings) {
+                if (!first_blend) launch_stage_blend(na, s);
+                first_blend = false;
+                bool admissible = true;
+                const double ta = now_ms();
+                residual_on(c, true);
+                int32_t bad = -1;
+                try {
+                    check_bad(c, &bad);
+                } catch (const Error& e) {
+                    if (e.code != ED_ELEMENT_INVERSION) throw;
+                    admissible = false;
+                }
+                st.t_assembly += 1e-3 * (now_ms() - ta);
+                if (admissible) {
+                    launch_kinematic_residual(c.d_fnode.p, c.nfree, c.m_udot.p, c.m_v.p, c.rk.p, s);
+                    dot(c.red, c.rk.p, c.rk.p, nvv, nr.p + 0, s);
+                    dot(c.red, c.rp.p, c.rp.p, N, nr.p + 1, s);
+                    dot(c.red, c.rm.p, c.rm.p, nvv, nr.p + 2, s);
+                    const std::vector<double> h = nr.to_host(s);
+                    norm = std::sqrt(h[0] + h[1] + h[2]);
+                    if (std::isfinite(norm) && norm <= kGrowthCap * norm_prev) break;
+                    admissible = false;
+                }
+                if (l == 1 || halvings >= 30) { // nothing to undo on the first pass
+                    st.converged = 0;
+                    goto done;
+                }
+                launch_halve(nh, s);
+            }
+            st.res_final = norm;
+            hist.push_back(norm);
+            norm_prev = norm;
+            if (l == 1) st.res0 = norm;
+            if (norm <= std::max(nl->tol_R * st.res0, nl->tol_A)) {
+                st.converged = 1;
+                goto done;
+            }
+            if (l > nl->l_max) break;
+            {
+                const double ta = now_ms();
+                tangent_on(c, true, *ts, true);
+                check_bad(c, nullptr);
+                ctx_planes_from_k4(c);
+                launch_rhs(c.rm.p, c.rp.p, c.fv.p, c.fp.p, static_cast<int>(nvv), N, chi, c.rhs.p, s);
+                c.sync();
+                st.t_assembly += 1e-3 * (now_ms() - ta);
+                const Stats ls = solve_block_system_dev(c, c.rhs.p, c.xsol.p, *opts, nullptr, nullptr);
+                lin.outer_iters += ls.outer_iters; // LinearStats::add (precond.hpp:30-41)
+                lin.a_solves += ls.a_solves;
+                lin.a_iters += ls.a_iters;
+                lin.s_solves += ls.s_solves;
+                lin.s_iters += ls.s_iters;
+                lin.schur_applies += ls.schur_applies;
+                lin.inner_iters += ls.inner_iters;
+                lin.converged = lin.converged && ls.converged;
+                lin.t_solve += ls.t_solve;
+                st.newton_iters += 1;
+                // prev = cur, then the two-stage update of cur (timeint.cpp:160-176)
+                keep(c.q_u, c.u);
+                keep(c.q_udot, c.udot);
+                keep(c.q_p, c.p);
+                keep(c.q_pdot, c.pdot);
+                keep(c.q_v, c.v);
+                keep(c.q_vdot, c.vdot);
+                launch_update(c.d_fnode.p, c.nfree, N, c.xsol.p, c.rk.p, chi, ts->alpha_m, gdt, c.u.p, c.udot.p,
+                              c.v.p, c.vdot.p, c.p.p, c.pdot.p, s);
+            }
+        }
+        st.converged = 0;
+    done:
+        c.sync();
+        st.n_res = static_cast<int32_t>(hist.size());
+        if (res_history)
+            for (int i = 0; i < res_cap && i < static_cast<int>(hist.size()); ++i) res_history[i] = hist[i];
+        if (out) *out = st;
+        fill_stats(lin, linear);
     });
 }
 

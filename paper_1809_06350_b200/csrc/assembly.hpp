@@ -77,6 +77,10 @@ struct NewtonArgs {
     double pf, alpha_m, alpha_f;
 };
 void launch_predict_blend(const NewtonArgs& a, cudaStream_t s);
+// mid = blend(yn, cur) (timeint.cpp:88-93)
+void launch_stage_blend(const NewtonArgs& a, cudaStream_t s);
+// cur = blend(prev, cur, 0.5) with prev in the yn_* slots (timeint.cpp:131-136)
+void launch_halve(const NewtonArgs& a, cudaStream_t s);
 // rk[r] = mid_udot[idx] - mid_v[idx] over free rows
 void launch_kinematic_residual(const int* fnode, int nfree, const double* mid_udot, const double* mid_v, double* rk,
                                cudaStream_t s);

@@ -168,6 +168,8 @@ struct Ctx {
     DevArray<double> m_u, m_udot, m_p, m_pdot, m_v, m_vdot; // stage state
     DevArray<double> rm, rp, fv, fp, rk, rhs, xsol;
     DevArray<double> s_u, s_udot, s_p, s_pdot, s_v, s_vdot; // saved state (benchmarks)
+    DevArray<double> y_u, y_udot, y_p, y_pdot, y_v, y_vdot; // y_n of a time step
+    DevArray<double> q_u, q_udot, q_p, q_pdot, q_v, q_vdot; // iterate before the last update (halving guard)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     DevArray<int> dscratch_i; // [0] bad element, [1] bad row
     // system

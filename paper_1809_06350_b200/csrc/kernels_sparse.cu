@@ -299,8 +299,10 @@ __global__ void __launch_bounds__(kThreads) k_sgs_flow(BsrArgs m, const double* 
         if (prev >= 0 && prev < nlev) {
             if (threadIdx.x == 0) {
                 const unsigned int need = static_cast<unsigned int>(lev_items[prev]);
-                while (ld_relaxed(done + prev) < need) __nanosleep(20);
-                (void)ld_acquire(done + prev);
+                // acquire on every poll: the satisfying poll is the acquire (one L2
+                // round trip less on the level's critical path than relaxed polling
+                // followed by a separate acquire load)
+                while (ld_acquire(done + prev) < need) __nanosleep(20);
             }
             __syncthreads();
         }

@@ -138,6 +138,41 @@ __global__ void k_predict_blend(NewtonArgs a)
     }
 }
 
+// stage blends only (timeint.cpp:88-93): mid = blend(yn, cur)
+__global__ void k_stage_blend(NewtonArgs a)
+{
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t n3 = 3 * static_cast<int64_t>(a.n_nodes);
+    if (i < n3) {
+        a.mid_udot[i] = a.yn_udot[i] + a.alpha_m * (a.cur_udot[i] - a.yn_udot[i]);
+        a.mid_vdot[i] = a.yn_vdot[i] + a.alpha_m * (a.cur_vdot[i] - a.yn_vdot[i]);
+        a.mid_u[i] = a.yn_u[i] + a.alpha_f * (a.cur_u[i] - a.yn_u[i]);
+        a.mid_v[i] = a.yn_v[i] + a.alpha_f * (a.cur_v[i] - a.yn_v[i]);
+    }
+    if (i < a.n_nodes) {
+        a.mid_pdot[i] = a.yn_pdot[i] + a.alpha_m * (a.cur_pdot[i] - a.yn_pdot[i]);
+        a.mid_p[i] = a.yn_p[i] + a.alpha_f * (a.cur_p[i] - a.yn_p[i]);
+    }
+}
+
+// admissibility guard (timeint.cpp:131-136): cur = blend(prev, cur, 0.5);
+// here the NewtonArgs' yn_* slots carry prev
+__global__ void k_halve(NewtonArgs a)
+{
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t n3 = 3 * static_cast<int64_t>(a.n_nodes);
+    if (i < n3) {
+        a.cur_udot[i] = a.yn_udot[i] + 0.5 * (a.cur_udot[i] - a.yn_udot[i]);
+        a.cur_vdot[i] = a.yn_vdot[i] + 0.5 * (a.cur_vdot[i] - a.yn_vdot[i]);
+        a.cur_u[i] = a.yn_u[i] + 0.5 * (a.cur_u[i] - a.yn_u[i]);
+        a.cur_v[i] = a.yn_v[i] + 0.5 * (a.cur_v[i] - a.yn_v[i]);
+    }
+    if (i < a.n_nodes) {
+        a.cur_pdot[i] = a.yn_pdot[i] + 0.5 * (a.cur_pdot[i] - a.yn_pdot[i]);
+        a.cur_p[i] = a.yn_p[i] + 0.5 * (a.cur_p[i] - a.yn_p[i]);
+    }
+}
+
 __global__ void k_kin_res(const int* __restrict__ fnode, int nfree, const double* __restrict__ udot,
                           const double* __restrict__ v, double* rk)
 {
@@ -219,6 +254,18 @@ void launch_predict_blend(const NewtonArgs& a, cudaStream_t s)
 {
     k_predict_blend<<<g1(3 * static_cast<int64_t>(a.n_nodes)), 256, 0, s>>>(a);
     after_launch("k_predict_blend");
+}
+
+void launch_stage_blend(const NewtonArgs& a, cudaStream_t s)
+{
+    k_stage_blend<<<g1(3 * static_cast<int64_t>(a.n_nodes)), 256, 0, s>>>(a);
+    after_launch("k_stage_blend");
+}
+
+void launch_halve(const NewtonArgs& a, cudaStream_t s)
+{
+    k_halve<<<g1(3 * static_cast<int64_t>(a.n_nodes)), 256, 0, s>>>(a);
+    after_launch("k_halve");
 }
 
 void launch_kinematic_residual(const int* fnode, int nfree, const double* mid_udot, const double* mid_v, double* rk,

@@ -331,3 +331,37 @@ def test_mid_cube_vcycle_and_newton_pass(oracle, n):
     _assert_stats(out["stats"], ro["stats"])
     _assert_history(out["history"], ro["history"])
     assert _rel(out["x"], ro["x"]) < X_TOL
+
+
+@pytest.mark.parametrize("case", ["cfg0_rest_5steps", "n8_seeded_2steps"])
+def test_time_steps_match_reference(oracle, case):
+    """step_generalized_alpha (timeint.cpp:40-180) -- Newton loop, growth
+    guard, convergence test -- over BASELINE configs[0] (5 steps from rest) and
+    a seeded 8^3 incompressible cube (2 steps): Newton counts, residual
+    histories, accumulated linear counts and the final state against the
+    reference."""
+    if case.startswith("cfg0"):
+        cp, steps, st = CubeProblem.config(0), 5, None
+    else:
+        cp, steps = CubeProblem(n=8, nu=0.5), 2
+        st = cp.seeded_state()
+    P = _ref_problem(oracle, cp)
+    ctx = cp.context(0)
+    if st is not None:
+        P.set_state(st.u, st.udot, st.p, st.pdot, st.v, st.vdot)
+        ctx.set_state(st)
+    opts = cp.solver_options()
+    for k in range(steps):
+        g = ctx.step(cp.ts, opts, tol_r=1e-8, tol_a=1e-6, l_max=20)
+        r = P.step(opts_to_ref(opts), tol_r=1e-8, tol_a=1e-6, l_max=20, t_n=k * cp.dt)
+        print(k, "gpu", g["newton_iters"], g["res_history"], g["linear"])
+        print(k, "ref", r["newton_iters"], r["res_history"], r["linear"])
+        assert g["converged"] == r["converged"]
+        assert abs(g["newton_iters"] - r["newton_iters"]) <= 1
+        h0 = r["res_history"][0]
+        n = min(len(g["res_history"]), len(r["res_history"]))
+        for i in range(n):
+            assert abs(g["res_history"][i] - r["res_history"][i]) <= 1e-8 * h0 + 1e-6 * r["res_history"][i], (k, i)
+        sg, sr = ctx.get_state(), P.get_state()
+        for key in ("u", "udot", "p", "pdot", "v", "vdot"):
+            assert _rel(getattr(sg, key), sr[key]) < 1e-7, (k, key, _rel(getattr(sg, key), sr[key]))
