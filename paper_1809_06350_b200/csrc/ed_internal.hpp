@@ -325,6 +325,8 @@ void bsr_scale(Bsr& M, const double* wr, const double* wc, cudaStream_t s);
 void bsr_diag(const Bsr& M, double* d, cudaStream_t s);
 // inv_diag[i] = d != 0 ? 1/d : 1
 void inv_diag_from(const double* d, double* invd, int64_t n, cudaStream_t s);
+// out[i] = 1 / d[i] (no guard)
+void recip(const double* d, double* out, int64_t n, cudaStream_t s);
 // z = Pinv r (dense n x n, row-major)
 void dense_gemv(const double* Pinv, const double* r, double* z, int n, cudaStream_t s);
 

@@ -568,6 +568,12 @@ __global__ void k_inv_diag(const double* __restrict__ d, double* invd, int64_t n
     if (i < n) invd[i] = d[i] != 0.0 ? 1.0 / d[i] : 1.0;
 }
 
+__global__ void k_recip(const double* __restrict__ d, double* out, int64_t n)
+{
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = 1.0 / d[i];
+}
+
 __global__ void k_jacobi(double* z, const double* __restrict__ b, const double* __restrict__ t,
                          const double* __restrict__ invd, double w, int64_t n)
 {
@@ -806,6 +812,13 @@ void inv_diag_from(const double* d, double* invd, int64_t n, cudaStream_t s)
     if (n == 0) return;
     k_inv_diag<<<static_cast<int>((n + kThreads - 1) / kThreads), kThreads, 0, s>>>(d, invd, n);
     after_launch("k_inv_diag");
+}
+
+void recip(const double* d, double* out, int64_t n, cudaStream_t s)
+{
+    if (n == 0) return;
+    k_recip<<<static_cast<int>((n + kThreads - 1) / kThreads), kThreads, 0, s>>>(d, out, n);
+    after_launch("k_recip");
 }
 
 void dense_gemv(const double* P, const double* r, double* z, int n, cudaStream_t s)

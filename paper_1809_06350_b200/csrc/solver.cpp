@@ -553,6 +553,66 @@ struct NestedPrec final : DPrec {
     void apply(const double* r, double* z) override { scr.solve(r, r + nv, z, z + nv); }
 };
 
+// SimplePrecond::apply, precond.cpp:122-155
+struct SimplePrec final : DPrec {
+    Ctx& c;
+    WorkSys& W;
+    KrylovCfg ta, ts;
+    DevHierarchy& amg_a;
+    DevHierarchy& amg_s;
+    Stats& st;
+    DevArray<double> invda, xhat, rp, t;
+    SimplePrec(Ctx& cc, WorkSys& w, const ed_block_solver_options& o, DevHierarchy& a, DevHierarchy& sh, Stats& sts)
+        : c(cc), W(w), ta(kcfg(o.a)), ts(kcfg(o.s)), amg_a(a), amg_s(sh), st(sts), invda(w.nv), xhat(w.nv),
+          rp(w.np), t(w.nv)
+    {
+        // inv_diag_a_ = 1 / diag(A) (precond.cpp:115-117, no zero guard)
+        bsr_diag(W.A, t.p, c.stream);
+        recip(t.p, invda.p, W.nv, c.stream);
+    }
+    void apply(const double* r, double* z) override
+    {
+        cudaStream_t s = c.stream;
+        MatOp aop(W.A, s), sop(W.S, s);
+        AmgPrec Ma(c, amg_a), Ms(c, amg_s);
+        // velocity predictor A xhat = r_v
+        vec_fill(xhat.p, 0.0, W.nv, s);
+        const SolveRes r1 = gmres_dev(c, aop, &Ma, r, xhat.p, ta, false, c.ws_a);
+        st.a_solves += 1;
+        st.a_iters += r1.iterations;
+        // pressure: S_hat x_p = r_p - C xhat
+        spmv(W.C, xhat.p, rp.p, r + W.nv, 1, s);
+        vec_fill(z + W.nv, 0.0, W.np, s);
+        const SolveRes r2 = gmres_dev(c, sop, &Ms, rp.p, z + W.nv, ts, false, c.ws_s);
+        st.s_solves += 1;
+        st.s_iters += r2.iterations;
+        // velocity correction z_v = xhat - inv_diag_a (B x_p)
+        spmv(W.B, z + W.nv, t.p, nullptr, 0, s);
+        vec_mul(t.p, invda.p, W.nv, s);
+        vec_sub_from(t.p, xhat.p, W.nv, s);
+        vec_copy(z, t.p, W.nv, s);
+    }
+};
+
+// JacobiPrecond on the monolithic (scaled) matrix (krylov.cpp:10-14)
+struct MonoJacobi final : DPrec {
+    Ctx& c;
+    int64_t n;
+    DevArray<double> invd;
+    MonoJacobi(Ctx& cc, WorkSys& W) : c(cc), n(static_cast<int64_t>(W.nv) + W.np), invd(n)
+    {
+        DevArray<double> d(n);
+        bsr_diag(W.A, d.p, c.stream);
+        bsr_diag(W.D, d.p + W.nv, c.stream);
+        inv_diag_from(d.p, invd.p, n, c.stream);
+    }
+    void apply(const double* r, double* z) override
+    {
+        vec_copy(z, r, n, c.stream);
+        vec_mul(z, invd.p, n, c.stream);
+    }
+};
+
 } // namespace
 
 AmgOpts amg_opts_from(const ed_amg_options& o, const Ctx& c, bool velocity, int nrows)
@@ -579,11 +639,14 @@ AmgOpts amg_opts_from(const ed_amg_options& o, const Ctx& c, bool velocity, int 
     return a;
 }
 
-// solve_block_system, precond.cpp:157-218 (Nested branch)
+// solve_block_system, precond.cpp:157-218: Nested (0), Simple (1), Jacobi
+// (3) and None (4); Ilu0 (2, a sequential triangular solve) is not built
 Stats solve_block_system_dev(Ctx& c, const double* d_rhs, double* d_x, const ed_block_solver_options& o,
                              std::vector<double>* history, ed_phase_times* times)
 {
-    if (o.precond != 0) throw Error(ED_UNSUPPORTED, "only the nested preconditioner is built (PrecondKind::Nested)");
+    if (o.precond == 2) throw Error(ED_UNSUPPORTED, "PrecondKind::Ilu0 is not built (sequential ILU(0) solves)");
+    if (o.precond < 0 || o.precond > 4) throw Error(ED_INVALID_ARGUMENT, "unknown PrecondKind");
+    const bool amg = o.precond == 0 || o.precond == 1;
     const double t0 = now_ms();
     cudaStream_t s = c.stream;
     Stats st;
@@ -598,7 +661,7 @@ Stats solve_block_system_dev(Ctx& c, const double* d_rhs, double* d_x, const ed_
     c.sync();
     const double t_planes = now_ms() - tp;
     tp = now_ms();
-    build_shat_work(c, W);
+    if (amg) build_shat_work(c, W);
     c.sync();
     const double t_shat = now_ms() - tp;
     tp = now_ms();
@@ -628,17 +691,17 @@ Stats solve_block_system_dev(Ctx& c, const double* d_rhs, double* d_x, const ed_
         omp_set_num_threads(prev_omp);
     };
     std::thread th;
-    if (!serial) th = std::thread(build_s);
+    if (amg && !serial) th = std::thread(build_s);
     try {
         const double t = now_ms();
-        amg_a.build(c, W.A, oa);
+        if (amg) amg_a.build(c, W.A, oa);
         ED_CUDA(cudaStreamSynchronize(c.stream));
         ms_a = now_ms() - t;
     } catch (...) {
         if (th.joinable()) th.join();
         throw;
     }
-    if (serial) build_s();
+    if (amg && serial) build_s();
     if (th.joinable()) th.join();
     static const bool tell = std::getenv("ED_SETUP_TIMES") != nullptr;
     if (tell) std::fprintf(stderr, "[setup] A %.1f ms  S %.1f ms\n", ms_a, ms_s);
@@ -646,10 +709,21 @@ Stats solve_block_system_dev(Ctx& c, const double* d_rhs, double* d_x, const ed_
     c.sync();
     const double t_amg = now_ms() - tp;
     tp = now_ms();
-    Scr scr(c, W, o, amg_a, amg_s, st);
-    NestedPrec M(scr, W.nv);
     BlockOp op(W, s);
-    const SolveRes res = gmres_dev(c, op, &M, b.p, d_x, kcfg(o.outer), true, c.ws_outer);
+    SolveRes res;
+    if (o.precond == 0) {
+        Scr scr(c, W, o, amg_a, amg_s, st);
+        NestedPrec M(scr, W.nv);
+        res = gmres_dev(c, op, &M, b.p, d_x, kcfg(o.outer), true, c.ws_outer);
+    } else if (o.precond == 1) {
+        SimplePrec M(c, W, o, amg_a, amg_s, st);
+        res = gmres_dev(c, op, &M, b.p, d_x, kcfg(o.outer), true, c.ws_outer);
+    } else if (o.precond == 3) {
+        MonoJacobi M(c, W);
+        res = gmres_dev(c, op, &M, b.p, d_x, kcfg(o.outer), false, c.ws_outer);
+    } else {
+        res = gmres_dev(c, op, nullptr, b.p, d_x, kcfg(o.outer), false, c.ws_outer);
+    }
     if (W.scaled) vec_mul(d_x, W.w.p, n, s);
     c.sync();
     const double t_fg = now_ms() - tp;
