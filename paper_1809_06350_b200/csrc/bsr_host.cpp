@@ -480,6 +480,8 @@ std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLay
     S.nnzb = pat.nnzb();
     const int n = pat.nbr;
     S.L = lanes > 0 ? lanes : auto_lanes(n > 0 ? static_cast<double>(S.nnzb) / n : 1.0, Rb * Cb);
+    // sweeps are latency-bound: as many lanes as blocks per row (shorter chains)
+    S.Ls = lanes > 0 ? lanes : auto_lanes(n > 0 ? static_cast<double>(S.nnzb) / n : 1.0, 9);
     S.h_rowptr.assign(n + 1, 0);
     S.h_col.assign(S.nnzb, 0);
     bool identity = true;
@@ -508,7 +510,7 @@ std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLay
     if (pat.nbr == pat.nbc) S.dpos.upload(dpos, s);
     // dataflow items: rows_per_item rows of one level each (256 threads / L lanes)
     const int nlev = S.nlev();
-    S.rows_per_item = 256 / S.L;
+    S.rows_per_item = 256 / S.Ls;
     std::vector<int> irow{0}, ilev, lcnt(std::max(nlev, 1), 0);
     for (int l = 0; l < nlev; ++l)
         for (int r0 = S.lev_ptr[l]; r0 < S.lev_ptr[l + 1]; r0 += S.rows_per_item) {
@@ -526,7 +528,7 @@ std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLay
     // narrow level schedules (every level fits one 512-thread CTA in <= 2 passes) run as one CTA
     int widest = 0;
     for (int l = 0; l < nlev; ++l) widest = std::max(widest, S.lev_ptr[l + 1] - S.lev_ptr[l]);
-    S.chain = static_cast<int64_t>(widest) * S.L <= 1024;
+    S.chain = static_cast<int64_t>(widest) * S.Ls <= 1024;
     // narrow, deep schedules whose vector fits in a cluster's shared memory
     // (<= 16 CTAs x 192 KB) run cluster-resident: z lives in DSMEM and a
     // cluster barrier separates levels

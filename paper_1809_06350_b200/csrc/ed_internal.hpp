@@ -162,7 +162,8 @@ struct BsrStruct {
     int Rb = 1, Cb = 1;
     int nbr = 0, nbc = 0; // block rows / block cols
     int64_t nnzb = 0;
-    int L = 8;            // lanes per block row
+    int L = 8;            // lanes per block row (SpMV)
+    int Ls = 8;           // lanes per block row of the Gauss-Seidel sweeps (latency-bound)
     DevArray<int> rowptr; // [nbr+1] over stored rows
     DevArray<int> col;    // [nnzb]
     DevArray<int> perm;   // [nbr] stored -> original (empty: identity)

@@ -682,7 +682,7 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
         return;
     }
     if (S.chain) {
-        ED_LANES(S.L, {
+        ED_LANES(S.Ls, {
             if (fwd)
                 k_sgs_chain<B, LL, true><<<1, 512, 0, s>>>(a, b, z, invd, S.d_lev_ptr.p, nlev);
             else
@@ -698,7 +698,7 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
     static bool traced = false;
     unsigned long long* tr = nullptr;
     if (!traced && fwd && nlev == trace_n) ED_CUDA(cudaMallocManaged(&tr, sizeof(unsigned long long) * 3 * S.nitems));
-    ED_LANES(S.L, {
+    ED_LANES(S.Ls, {
         if (fwd)
             k_sgs_flow<B, LL, true><<<grid, kThreads, 0, s>>>(a, b, z, invd, S.nitems, nlev, S.item_row.p,
                                                              S.item_level.p, S.lev_items.p, S.sync.p, tr);
