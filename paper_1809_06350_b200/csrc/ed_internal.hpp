@@ -331,6 +331,21 @@ void recip(const double* d, double* out, int64_t n, cudaStream_t s);
 // z = Pinv r (dense n x n, row-major)
 void dense_gemv(const double* Pinv, const double* r, double* z, int n, cudaStream_t s);
 
+// ---- ILU(0) on the monolithic block system (ilu0.cu) ----
+struct WorkSysView {
+    const Bsr *A, *B, *C, *D;
+};
+struct DevIlu0 {
+    int n = 0, nlf = 0, nlb = 0;
+    DevArray<int> rowptr, col, dpos, lf_ptr, rows_f, lb_ptr, rows_b;
+    DevArray<double> val; // factors: unit-lower L below the diagonal, U on and above
+};
+// Ilu0Precond(monolithic_csr(K)) (ilu0.cpp:9-48): throws ED_ZERO_DIAGONAL on a
+// missing diagonal or a zero pivot
+void ilu0_build(const WorkSysView& W, DevIlu0& f, cudaStream_t s);
+// z = U^-1 L^-1 r (ilu0.cpp:50-68)
+void ilu0_apply(const DevIlu0& f, const double* r, double* z, cudaStream_t s);
+
 // ---- vectors / reductions (deterministic: fixed grid, fixed order) ----
 void vec_fill(double* x, double v, int64_t n, cudaStream_t s);
 void vec_copy(double* y, const double* x, int64_t n, cudaStream_t s);

@@ -613,6 +613,14 @@ struct MonoJacobi final : DPrec {
     }
 };
 
+// Ilu0Precond on the monolithic (scaled) matrix (ilu0.cpp)
+struct IluPrec final : DPrec {
+    Ctx& c;
+    DevIlu0 f;
+    IluPrec(Ctx& cc, WorkSys& W) : c(cc) { ilu0_build(WorkSysView{&W.A, &W.B, &W.C, &W.D}, f, c.stream); }
+    void apply(const double* r, double* z) override { ilu0_apply(f, r, z, c.stream); }
+};
+
 } // namespace
 
 AmgOpts amg_opts_from(const ed_amg_options& o, const Ctx& c, bool velocity, int nrows)
@@ -639,12 +647,11 @@ AmgOpts amg_opts_from(const ed_amg_options& o, const Ctx& c, bool velocity, int 
     return a;
 }
 
-// solve_block_system, precond.cpp:157-218: Nested (0), Simple (1), Jacobi
-// (3) and None (4); Ilu0 (2, a sequential triangular solve) is not built
+// solve_block_system, precond.cpp:157-218: Nested (0), Simple (1), Ilu0 (2),
+// Jacobi (3) and None (4)
 Stats solve_block_system_dev(Ctx& c, const double* d_rhs, double* d_x, const ed_block_solver_options& o,
                              std::vector<double>* history, ed_phase_times* times)
 {
-    if (o.precond == 2) throw Error(ED_UNSUPPORTED, "PrecondKind::Ilu0 is not built (sequential ILU(0) solves)");
     if (o.precond < 0 || o.precond > 4) throw Error(ED_INVALID_ARGUMENT, "unknown PrecondKind");
     const bool amg = o.precond == 0 || o.precond == 1;
     const double t0 = now_ms();
@@ -718,6 +725,9 @@ Stats solve_block_system_dev(Ctx& c, const double* d_rhs, double* d_x, const ed_
     } else if (o.precond == 1) {
         SimplePrec M(c, W, o, amg_a, amg_s, st);
         res = gmres_dev(c, op, &M, b.p, d_x, kcfg(o.outer), true, c.ws_outer);
+    } else if (o.precond == 2) {
+        IluPrec M(c, W);
+        res = gmres_dev(c, op, &M, b.p, d_x, kcfg(o.outer), false, c.ws_outer);
     } else if (o.precond == 3) {
         MonoJacobi M(c, W);
         res = gmres_dev(c, op, &M, b.p, d_x, kcfg(o.outer), false, c.ws_outer);

@@ -367,18 +367,19 @@ def test_time_steps_match_reference(oracle, case):
             assert _rel(getattr(sg, key), sr[key]) < 1e-7, (k, key, _rel(getattr(sg, key), sr[key]))
 
 
-@pytest.mark.parametrize("kind", [1, 3, 4])
+@pytest.mark.parametrize("kind", [1, 2, 3, 4])
 def test_solve_block_system_variants(cfg0, oracle, kind):
     """solve_block_system's other PrecondKinds (precond.cpp:157-218): Simple
-    (FGMRES + SimplePrecond, :111-155), Jacobi (GMRES + monolithic
-    JacobiPrecond) and None (plain GMRES) against the reference."""
+    (FGMRES + SimplePrecond, :111-155), Ilu0 (GMRES + Ilu0Precond on the
+    monolithic matrix), Jacobi (GMRES + monolithic JacobiPrecond) and None
+    (plain GMRES) against the reference."""
     cp, P, st, planes = cfg0
     ctx = api.Context(0)
     ctx.set_block_system(*[_csr(m) for m in planes])
     rhs = np.random.default_rng(40 + kind).uniform(-1, 1, cp.nv + cp.np)
     opts = cp.solver_options()
     opts.precond = kind
-    if kind in (3, 4):
+    if kind in (2, 3, 4):
         opts.outer = api.krylov_config(100, 400, 1e-4)
     xg, sg, hg = ctx.solve_block_system(rhs, opts)
     xr, sr, hr = P.solve_tangent(rhs, opts_to_ref(opts))
