@@ -335,29 +335,41 @@ __global__ void k_unique_write_warp(const int* __restrict__ keys, const int* __r
 // entries of B row K are split across lanes (distinct C columns inside one B
 // row), and __syncwarp orders consecutive K steps, so every C entry still
 // receives its products in csr_matmul's traversal order.
+constexpr int kWarpsPerCta = 8;  // kT / 32
+constexpr int kWarpCols = 1024;   // C row columns staged per warp (4 KB)
+
 template <int RA, int KA, int CB>
 __global__ void k_spgemm_numeric_warp(const int* __restrict__ arp, const int* __restrict__ acol,
                                       const double* __restrict__ aval, const int* __restrict__ brp,
                                       const int* __restrict__ bcol, const double* __restrict__ bval,
                                       const int* __restrict__ crp, const int* __restrict__ ccol, double* cval, int n)
 {
+    // the C row's column list staged in shared memory (binary searches on
+    // shared instead of global memory) when it fits kWarpCols
+    __shared__ int s_cols[kWarpsPerCta][kWarpCols];
     const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int I = static_cast<int>(w / RA), c = static_cast<int>(w % RA);
     if (I >= n) return;
-    const int c0 = crp[I], c1 = crp[I + 1];
+    const int c0 = crp[I], c1 = crp[I + 1], nc = c1 - c0;
+    const bool cached = nc <= kWarpCols;
+    const int* cc = cached ? s_cols[wib] : ccol + c0;
+    if (cached) {
+        for (int t = lane; t < nc; t += 32) s_cols[wib][t] = ccol[c0 + t];
+        __syncwarp();
+    }
     for (int k = arp[I]; k < arp[I + 1]; ++k) {
         const int K = acol[k];
         const int b0 = brp[K], b1 = brp[K + 1];
         for (int kb = b0 + lane; kb < b1; kb += 32) {
             const int J = bcol[kb];
-            int lo = c0, hi = c1;
+            int lo = 0, hi = nc;
             while (lo < hi) {
                 const int mid = lo + ((hi - lo) >> 1);
-                if (ccol[mid] < J) lo = mid + 1;
+                if (cc[mid] < J) lo = mid + 1;
                 else hi = mid;
             }
-            double* cv = cval + static_cast<int64_t>(lo) * RA * CB + c * CB;
+            double* cv = cval + static_cast<int64_t>(c0 + lo) * RA * CB + c * CB;
 #pragma unroll
             for (int d = 0; d < KA; ++d) {
                 const double a = aval[static_cast<int64_t>(k) * RA * KA + c * KA + d];
