@@ -230,10 +230,35 @@ def spmv_leg(n, device, peak):
     for name, (ms, by) in k.items():
         gbs = by / (ms * 1e-3) / 1e9
         out[name] = {"ms": ms, "bytes": by, "achieved_gbs": gbs, "frac": gbs / peak}
+    out["assembly"] = assembly_row(ctx.bench_assembly(cp.ts, n_rep=3), peak)
     ctx.close()
     del ctx, cp
     gc.collect()
     return out
+
+
+# FP64 flops per element of the tangent (element kernel + fold-in) and the
+# residual kernels: ncu sm__sass_thread_inst_executed_op_{dadd,dmul,dfma}
+# (fma = 2) of one launch over its elements (profiles/r01c_assembly_ncu.md)
+TANGENT_FLOP_PER_ELEM = None
+RESIDUAL_FLOP_PER_ELEM = None
+
+
+def assembly_row(a, peak):
+    """Assembly at the metric's size: Melem/s, algorithmic GB/s
+    against HBM, FP64 rate against the measured FMA peak."""
+    E = a["elements"]
+    row = {"elements": E, "fp64_peak_gflops_measured": a["fp64_peak_gflops"],
+           "k4_staging_bytes": a["k4_bytes"], "plane_bytes": a["plane_bytes"]}
+    for part, fpe in (("residual", RESIDUAL_FLOP_PER_ELEM), ("tangent", TANGENT_FLOP_PER_ELEM)):
+        ms, by = a[f"{part}_ms"], a[f"{part}_bytes"]
+        r = {"ms": ms, "melem_s": E / (ms * 1e-3) / 1e6, "bytes": by, "achieved_gbs": by / (ms * 1e-3) / 1e9,
+             "hbm_frac": by / (ms * 1e-3) / 1e9 / peak}
+        if fpe:
+            r["fp64_gflops"] = fpe * E / (ms * 1e-3) / 1e9
+            r["fp64_frac"] = r["fp64_gflops"] / a["fp64_peak_gflops"]
+        row[part] = r
+    return row
 
 
 def _profiler_range():
@@ -348,6 +373,15 @@ def run_ours(args, world, rank, local, dist):
                       "share_of_step": (kms / args.steps) / step_ms, "bytes_per_launch": kbytes / max(n_l, 1),
                       "ms_per_launch": kms / max(n_l, 1), "achieved_gbs": kbytes / (kms * 1e-3) / 1e9 if kms > 0 else 0.0}
     live = dict(sorted(live.items(), key=lambda kv: -kv[1]["ms_per_step"]))
+    # SURVEY.md 8d solve roofline: algorithmic bytes of every accounted launch of
+    # the solve (SpMV, sweeps, dense GEMV, Krylov vector kernels) / HBM peak,
+    # against the measured FGMRES time (AMG setup excluded, reported beside it)
+    solve_bytes = sum(kbytes for (_, _, kbytes) in acct.values()) / args.steps
+    fg_ms = sum(p["fgmres_ms"] for p in phase) / len(phase)
+    solve_roof = {"bytes_per_step": solve_bytes, "time_roof_ms": solve_bytes / (peak * 1e9) * 1e3,
+                  "fgmres_ms": fg_ms, "frac": solve_bytes / (peak * 1e9) * 1e3 / fg_ms,
+                  "time_roof_ms_8tbs": solve_bytes / 8e12 * 1e3,
+                  "amg_setup_ms": sum(p["amg_setup_ms"] for p in phase) / len(phase)}
     top = next(iter(live)) if live else None
     head = live[top] if top else {"achieved_gbs": 0.0}
     traffic = _ncu_traffic(top)
@@ -373,7 +407,8 @@ def run_ours(args, world, rank, local, dist):
                      "traffic": traffic,
                      "note": ("Gauss-Seidel half sweeps keep the reference's sequential semantics: their time is "
                               "dependency levels x per-level latency, not bytes (DESIGN.md §4)"),
-                     "live_kernels": dict(list(live.items())[:10]), "standalone_kernels": micro},
+                     "live_kernels": dict(list(live.items())[:10]), "standalone_kernels": micro,
+                     "solve": solve_roof},
         "spmv_cfg4": spmv,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -252,6 +252,12 @@ int ed_timer(ed_ctx* ctx, int op, float* ms);
  * bytes per launch, for k = 0 coupled K x, 1 A-plane SpMV, 2 fine-level
  * Gauss-Seidel forward sweep on A, 3 S_hat SpMV. */
 int ed_bench_kernels(ed_ctx* ctx, const ed_block_solver_options* opts, int n_rep, double* out);
+/* Device-timed assembly (after one ed_assemble_tangent): out[0] residual ms
+ * (element kernels + tractions), out[1] its algorithmic bytes, out[2] tangent ms
+ * (element kernels with the fold-in + BSR planes), out[3] its algorithmic bytes,
+ * out[4] measured FP64 FMA peak GFLOP/s, out[5] elements, out[6] plane bytes,
+ * out[7] K4 staging bytes. */
+int ed_bench_assembly(ed_ctx* ctx, const ed_time_scalars* ts, int n_rep, double* out);
 /* Live kernel accounting: while on, every sparse launch (SpMV, Gauss-Seidel
  * half sweep) is bracketed by CUDA events on its stream and attributed to
  * "kernel@level" with its algorithmic bytes.  on = 1 clears the totals. */

@@ -27,7 +27,7 @@ EXPORTED = [
     "ed_foldin_download", "ed_block_system_upload", "ed_solve_block_system",
     "ed_solve_block_system_device", "ed_newton_first_pass", "ed_step_generalized_alpha", "ed_block_matvec", "ed_gmres_a",
     "ed_amg_vcycle", "ed_shat_export", "ed_block_matvec_device", "ed_spmv_bytes", "ed_state_save",
-    "ed_state_restore", "ed_timer", "ed_bench_kernels", "ed_kernel_accounting", "ed_kernel_account_count",
+    "ed_state_restore", "ed_timer", "ed_bench_kernels", "ed_bench_assembly", "ed_kernel_accounting", "ed_kernel_account_count",
     "ed_kernel_account_get",
 ]
 
@@ -156,6 +156,7 @@ def lib():
         "ed_state_restore": (C.c_int, [P]),
         "ed_timer": (C.c_int, [P, C.c_int, C.POINTER(C.c_float)]),
         "ed_bench_kernels": (C.c_int, [P, C.POINTER(BlockSolverOptions), C.c_int, dp]),
+        "ed_bench_assembly": (C.c_int, [P, C.POINTER(TimeScalars), C.c_int, dp]),
         "ed_kernel_accounting": (C.c_int, [P, C.c_int]),
         "ed_kernel_account_count": (C.c_int, [P, C.POINTER(C.c_int)]),
         "ed_kernel_account_get": (C.c_int, [P, C.c_int, C.c_char_p, C.c_int, C.POINTER(_i64), dp, dp]),

@@ -393,6 +393,15 @@ class Context:
         names = ("coupled_spmv", "a_spmv", "sgs_fwd_fine", "shat_spmv")
         return {k: (float(out[2 * i]), float(out[2 * i + 1])) for i, k in enumerate(names)}
 
+    def bench_assembly(self, ts, n_rep=5):
+        """Device-timed residual and tangent assembly (after assemble_tangent):
+        ms, algorithmic bytes, the FP64 FMA peak GFLOP/s."""
+        out = np.zeros(8)
+        self._chk(N.lib().ed_bench_assembly(self._p, C.byref(ts), n_rep, N.dp(out)))
+        return {"residual_ms": float(out[0]), "residual_bytes": float(out[1]), "tangent_ms": float(out[2]),
+                "tangent_bytes": float(out[3]), "fp64_peak_gflops": float(out[4]), "elements": int(out[5]),
+                "plane_bytes": float(out[6]), "k4_bytes": float(out[7])}
+
     def kernel_accounting(self, on: bool):
         """Bracket every sparse launch with CUDA events (bench.py roofline)."""
         self._chk(N.lib().ed_kernel_accounting(self._p, int(on)))

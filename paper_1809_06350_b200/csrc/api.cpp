@@ -101,22 +101,38 @@ struct Acct {
         open.clear();
     }
 } g_acct;
+std::mutex g_acct_mu;
 } // namespace
 
 bool acct_on() { return g_acct.on; }
 
-void acct_begin(cudaStream_t s, const char* name, double bytes)
+// concurrent hierarchy builds run on their own host threads: records are
+// appended under a lock and a scope closes its own record (by index); records
+// are resolved only at the API's synchronisation points (ed_kernel_account*)
+int acct_begin(cudaStream_t s, const char* name, double bytes)
 {
-    if (g_acct.open.size() >= 8192) g_acct.flush(); // before the push: acct_end pairs with open.back()
+    std::lock_guard<std::mutex> lk(g_acct_mu);
+    if (g_acct.open.size() >= (1u << 20)) return -1;
     Acct::Rec r{prof_tag().empty() ? std::string(name) : std::string(name) + "@" + prof_tag(), bytes, g_acct.get(),
                 g_acct.get()};
     ED_CUDA(cudaEventRecord(r.a, s));
     g_acct.open.push_back(r);
+    return static_cast<int>(g_acct.open.size()) - 1;
 }
 
-void acct_end(cudaStream_t s)
+void acct_end(cudaStream_t s, int idx)
 {
-    if (!g_acct.open.empty()) ED_CUDA(cudaEventRecord(g_acct.open.back().b, s));
+    std::lock_guard<std::mutex> lk(g_acct_mu);
+    if (idx >= 0 && idx < static_cast<int>(g_acct.open.size())) ED_CUDA(cudaEventRecord(g_acct.open[idx].b, s));
+}
+
+// bytes only (no events): the Krylov vector kernels, for the solve roofline
+void acct_bytes(const char* name, double bytes)
+{
+    std::lock_guard<std::mutex> lk(g_acct_mu);
+    Acct::Tot& t = g_acct.tot[prof_tag().empty() ? std::string(name) : std::string(name) + "@" + prof_tag()];
+    t.n += 1;
+    t.bytes += bytes;
 }
 
 namespace {
@@ -1213,6 +1229,71 @@ int ed_bench_kernels(ed_ctx* ctx, const ed_block_solver_options* opts, int n_rep
     });
 }
 
+
+int ed_bench_assembly(ed_ctx* ctx, const ed_time_scalars* ts, int n_rep, double* out)
+{
+    return guarded(ctx, [&](Ctx& c) {
+        check(ts && out && n_rep > 0, ED_INVALID_ARGUMENT, "bad arguments");
+        check(c.have_dofs && c.have_mat && c.sys_from_mesh, ED_NOT_READY, "assemble the tangent once first");
+        cudaEvent_t e0, e1;
+        ED_CUDA(cudaEventCreate(&e0));
+        ED_CUDA(cudaEventCreate(&e1));
+        auto time = [&](auto&& f) {
+            f(); // warm
+            ED_CUDA(cudaEventRecord(e0, c.stream));
+            for (int r = 0; r < n_rep; ++r) f();
+            ED_CUDA(cudaEventRecord(e1, c.stream));
+            ED_CUDA(cudaEventSynchronize(e1));
+            float t = 0.0f;
+            ED_CUDA(cudaEventElapsedTime(&t, e0, e1));
+            return static_cast<double>(t) / n_rep;
+        };
+        if (c.rk.n < 3 * static_cast<size_t>(c.nfree)) { // fold-in with a zero kinematic residual
+            c.rk.alloc(3 * static_cast<size_t>(c.nfree));
+            c.rk.zero(c.stream);
+        }
+        reset_bad(c);
+        AsmArgs A = asm_args(c, false);
+        A.ts = *ts;
+        A.rk = c.rk.p;
+        // residual: zero R, element kernels, tractions (residual_on without its host sync)
+        out[0] = time([&] {
+            c.rm.zero(c.stream);
+            c.rp.zero(c.stream);
+            launch_residual(A, c.color_ptr, c.stream);
+            launch_traction(c.tr_rowptr.p, c.tr_rows.p, c.tr_vals.p, c.tr_n, c.rm.p, c.stream);
+        });
+        // tangent with the fold-in, K4 staging and the four BSR planes
+        out[2] = time([&] {
+            c.k4.zero(c.stream);
+            c.fv.zero(c.stream);
+            c.fp.zero(c.stream);
+            launch_tangent(A, c.color_ptr, c.stream);
+            ctx_planes_from_k4(c);
+        });
+        check_bad(c, nullptr);
+        // algorithmic bytes: per element connectivity 16 B + grad N / volume / tau 112 B;
+        // state 11 doubles per node; outputs written once
+        const double E = c.n_tets, Nn = c.n_nodes, nv = 3.0 * c.nfree, np = c.n_nodes;
+        const BlockSys& S = c.sys;
+        const double planes = S.A.st->nnzb * 8.0 * S.Bv * S.Bv + S.B.st->nnzb * 8.0 * S.Bv +
+                              S.C.st->nnzb * 8.0 * S.Bv + S.D.st->nnzb * 8.0;
+        out[1] = 128.0 * E + 88.0 * Nn + 8.0 * (nv + np);
+        out[3] = 128.0 * E + 88.0 * Nn + 8.0 * nv + planes + 8.0 * (nv + np);
+        // FP64 FMA peak of this device (2 flops per fma)
+        DevArray<double> sink(1);
+        const int iters = 1 << 14;
+        const double fl = launch_fp64_fma(sink.p, iters, c.stream);
+        const double ms = time([&] { launch_fp64_fma(sink.p, iters, c.stream); });
+        out[4] = fl / (ms * 1e-3) / 1e9;
+        out[5] = E;
+        out[6] = planes;
+        out[7] = static_cast<double>(c.k4.n) * 8.0; // K4 staging array bytes (written once, read once)
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    });
+}
+
 } // extern "C"
 
 extern "C" {
@@ -1221,6 +1302,7 @@ int ed_kernel_accounting(ed_ctx* ctx, int on)
 {
     return guarded(ctx, [&](Ctx& c) {
         c.sync();
+        std::lock_guard<std::mutex> lk(g_acct_mu);
         g_acct.flush();
         if (on) g_acct.tot.clear();
         g_acct.on = on != 0;
@@ -1232,6 +1314,7 @@ int ed_kernel_account_count(ed_ctx* ctx, int* n)
     return guarded(ctx, [&](Ctx& c) {
         check(n != nullptr, ED_INVALID_ARGUMENT, "null count");
         c.sync();
+        std::lock_guard<std::mutex> lk(g_acct_mu);
         g_acct.flush();
         *n = static_cast<int>(g_acct.tot.size());
     });

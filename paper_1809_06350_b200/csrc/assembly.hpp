@@ -30,6 +30,8 @@ void launch_residual(const AsmArgs& A, const std::vector<int>& color_ptr, cudaSt
 void launch_tangent(const AsmArgs& A, const std::vector<int>& color_ptr, cudaStream_t s);
 void launch_traction(const int64_t* rowptr, const int* rows, const double* vals, int nrows_with, double* r_m,
                      cudaStream_t s);
+// FP64 FMA probe: returns the flops of one launch
+double launch_fp64_fma(double* out, int iters, cudaStream_t s);
 void launch_k4_to_plane(int plane, const int* src, const double* k4, double* val, int64_t nnzb, cudaStream_t s);
 
 // ---- system kernels (kernels_system.cu) ----

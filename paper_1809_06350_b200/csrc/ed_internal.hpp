@@ -389,18 +389,24 @@ namespace edb {
 // Live per-kernel accounting (bench.py's roofline): CUDA events around each
 // sparse launch on its stream, resolved after the caller synchronises.
 bool acct_on();
-void acct_begin(cudaStream_t s, const char* name, double bytes);
-void acct_end(cudaStream_t s);
+int acct_begin(cudaStream_t s, const char* name, double bytes);
+void acct_end(cudaStream_t s, int idx);
+void acct_bytes(const char* name, double bytes);
 struct AcctScope {
     cudaStream_t s;
-    bool on;
-    AcctScope(cudaStream_t st, const char* name, double bytes) : s(st), on(acct_on())
+    int idx = -1;
+    AcctScope(cudaStream_t st, const char* name, double bytes) : s(st)
     {
-        if (on) acct_begin(s, name, bytes);
+        if (acct_on()) idx = acct_begin(s, name, bytes);
     }
     ~AcctScope()
     {
-        if (on) acct_end(s);
+        if (idx >= 0) acct_end(s, idx);
     }
 };
+// algorithmic bytes of a launch whose time is not recorded (vector kernels)
+inline void acct_vec(const char* name, double bytes)
+{
+    if (acct_on()) acct_bytes(name, bytes);
+}
 } // namespace edb

@@ -17,6 +17,9 @@
 // unstable sort (csr.cpp:84-87), hence parity is at roundoff level.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <mutex>
+
 #include "ed_internal.hpp"
 #include "assembly.hpp"
 
@@ -188,11 +191,15 @@ struct Frame {
 // ptilde_dir (materials.cpp:108-129) for dF = e_j (x) G_b
 __device__ void ptilde_dir(const ed_material& m, const Frame& f, int bn, int j, double* out)
 {
+    // dF = e_j (x) G_b, built with selects (no dynamically indexed local array)
     double dF[9];
+    const double g0 = f.G[bn][0], g1 = f.G[bn][1], g2 = f.G[bn][2];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) dF[k] = 0.0;
-#pragma unroll
-    for (int J2 = 0; J2 < 3; ++J2) dF[3 * j + J2] = f.G[bn][J2];
+    for (int r = 0; r < 3; ++r) {
+        dF[3 * r + 0] = r == j ? g0 : 0.0;
+        dF[3 * r + 1] = r == j ? g1 : 0.0;
+        dF[3 * r + 2] = r == j ? g2 : 0.0;
+    }
     // t = ddot3(transpose3(Finv), dF)
     double FinvT[9] = {f.Finv[0], f.Finv[3], f.Finv[6], f.Finv[1], f.Finv[4], f.Finv[7],
                        f.Finv[2], f.Finv[5], f.Finv[8]};
@@ -369,7 +376,8 @@ __device__ void build_frame(const AsmArgs& A, Frame& f, int e, int lane, bool ac
 }
 
 // Residual kernel: lane = 4a + c, c < 3 -> R_m[a][c], c == 3 -> R_p[a].
-__global__ void __launch_bounds__(kCta) k_residual(AsmArgs A, int c0, int count)
+template <int MINB>
+__global__ void __launch_bounds__(kCta, MINB) k_residual(AsmArgs A, int c0, int count)
 {
     __shared__ Frame frames[kTeamsPerCta];
     const int team = threadIdx.x / kTeam;
@@ -410,7 +418,8 @@ __global__ void __launch_bounds__(kCta) k_residual(AsmArgs A, int c0, int count)
 
 // Tangent kernel: dP for 12 directions, then lane = 4a + bn forms node block
 // (a, bn) of eA, eB, eC, eD (+ eM, eK for the fold-in).
-__global__ void __launch_bounds__(kCta) k_tangent(AsmArgs A, int c0, int count)
+template <int MINB>
+__global__ void __launch_bounds__(kCta, MINB) k_tangent(AsmArgs A, int c0, int count)
 {
     __shared__ Frame frames[kTeamsPerCta];
     const int team = threadIdx.x / kTeam;
@@ -575,22 +584,72 @@ __global__ void k_k4_to_plane(const int* __restrict__ src, const double* __restr
 
 } // namespace
 
+// resident CTAs per SM the element kernels are compiled for (register cap);
+// ED_ASM_MINB=<residual><tangent> picks a variant (experiments), e.g. 86
+int asm_minb(int which)
+{
+    // measured at 160^3 (profiles/r01c_assembly.md): residual 8 CTAs/SM (64
+    // registers), tangent 4 (128 registers, no spills)
+    const char* e = std::getenv("ED_ASM_MINB");
+    const int v = e ? std::atoi(e) : 84;
+    return which == 0 ? v / 10 : v % 10;
+}
+
+// the frames are 22 KB of static shared memory per CTA: ask for the largest
+// shared-memory carveout so the register cap, not the carveout, sets residency
+template <typename K>
+void max_carveout(K kernel)
+{
+    ED_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared));
+}
+
+#define ED_ASM_LAUNCH(KER, MB, ...)                                                                            \
+    switch (MB) {                                                                                              \
+    case 4: KER<4><<<__VA_ARGS__>>>(A, color_ptr[c], count); break;                                           \
+    case 5: KER<5><<<__VA_ARGS__>>>(A, color_ptr[c], count); break;                                           \
+    case 6: KER<6><<<__VA_ARGS__>>>(A, color_ptr[c], count); break;                                           \
+    case 8: KER<8><<<__VA_ARGS__>>>(A, color_ptr[c], count); break;                                           \
+    default: KER<1><<<__VA_ARGS__>>>(A, color_ptr[c], count); break;                                          \
+    }
+
+void carveouts()
+{
+    static std::once_flag once;
+    std::call_once(once, [] {
+        max_carveout(k_residual<1>);
+        max_carveout(k_residual<4>);
+        max_carveout(k_residual<5>);
+        max_carveout(k_residual<6>);
+        max_carveout(k_residual<8>);
+        max_carveout(k_tangent<1>);
+        max_carveout(k_tangent<4>);
+        max_carveout(k_tangent<5>);
+        max_carveout(k_tangent<6>);
+        max_carveout(k_tangent<8>);
+    });
+}
+
 void launch_residual(const AsmArgs& A, const std::vector<int>& color_ptr, cudaStream_t s)
 {
+    carveouts();
+    const int mb = asm_minb(0);
     for (size_t c = 0; c + 1 < color_ptr.size(); ++c) {
         const int count = color_ptr[c + 1] - color_ptr[c];
         if (count == 0) continue;
-        k_residual<<<(count + kTeamsPerCta - 1) / kTeamsPerCta, kCta, 0, s>>>(A, color_ptr[c], count);
+        ED_ASM_LAUNCH(k_residual, mb, (count + kTeamsPerCta - 1) / kTeamsPerCta, kCta, 0, s)
         after_launch("k_residual");
     }
 }
 
 void launch_tangent(const AsmArgs& A, const std::vector<int>& color_ptr, cudaStream_t s)
 {
+    carveouts();
+    const int mb = asm_minb(1);
     for (size_t c = 0; c + 1 < color_ptr.size(); ++c) {
         const int count = color_ptr[c + 1] - color_ptr[c];
         if (count == 0) continue;
-        k_tangent<<<(count + kTeamsPerCta - 1) / kTeamsPerCta, kCta, 0, s>>>(A, color_ptr[c], count);
+        ED_ASM_LAUNCH(k_tangent, mb, (count + kTeamsPerCta - 1) / kTeamsPerCta, kCta, 0, s)
         after_launch("k_tangent");
     }
 }

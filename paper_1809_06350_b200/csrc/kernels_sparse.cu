@@ -825,6 +825,7 @@ void dense_gemv(const double* P, const double* r, double* z, int n, cudaStream_t
 {
     if (n == 0) return;
     const int rows_per_block = kThreads / 32;
+    acct_vec("k_dense_gemv", 8.0 * n * n + 16.0 * n);
     k_dense_gemv<<<(n + rows_per_block - 1) / rows_per_block, kThreads, 0, s>>>(P, r, z, n);
     after_launch("k_dense_gemv");
 }

@@ -292,4 +292,33 @@ void launch_update(const int* fnode, int nfree, int np, const double* x, const d
     after_launch("k_update");
 }
 
+
+// FP64 FMA throughput probe (bench.py's assembly roofline denominator):
+// 8 independent fma chains per thread, 4 resident CTAs of 256 per SM.
+__global__ void __launch_bounds__(256) k_fp64_fma(double* out, int iters, double a, double b)
+{
+    double x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = threadIdx.x * 1e-3 + j;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = fma(x[j], a, b);
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc += x[j];
+    if (acc == 1.2345e300) out[0] = acc; // keep the chains live
+}
+
+double launch_fp64_fma(double* out, int iters, cudaStream_t s)
+{
+    int dev = 0, sms = 0;
+    ED_CUDA(cudaGetDevice(&dev));
+    ED_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int blocks = sms * 8;
+    k_fp64_fma<<<blocks, 256, 0, s>>>(out, iters, 0.999999, 1e-7);
+    after_launch("k_fp64_fma");
+    return 2.0 * 8.0 * static_cast<double>(iters) * blocks * 256;
+}
+
 } // namespace edb

@@ -251,6 +251,7 @@ void Reducer::ensure(int vals, cudaStream_t s)
 void dot(Reducer& R, const double* x, const double* y, int64_t n, double* out, cudaStream_t s)
 {
     R.ensure(1, s);
+    acct_vec("k_dot", 16.0 * n);
     k_dot<false><<<reduce_blocks(n), kRT, 0, s>>>(x, y, n, R.partials.p, R.ticket.p, out);
     after_launch("k_dot");
 }
@@ -258,6 +259,7 @@ void dot(Reducer& R, const double* x, const double* y, int64_t n, double* out, c
 void norm2(Reducer& R, const double* x, int64_t n, double* out, cudaStream_t s)
 {
     R.ensure(1, s);
+    acct_vec("k_norm", 8.0 * n);
     k_dot<true><<<reduce_blocks(n), kRT, 0, s>>>(x, x, n, R.partials.p, R.ticket.p, out);
     after_launch("k_norm");
 }
@@ -266,6 +268,7 @@ void mgs_axpy_dot(Reducer& R, double* w, const double* vprev, const double* hpre
                   int64_t n, double* hout, cudaStream_t s)
 {
     R.ensure(1, s);
+    acct_vec("k_mgs", 32.0 * n);
     k_mgs<<<reduce_blocks(n), kRT, 0, s>>>(w, vprev, hprev, vnext, n, R.partials.p, R.ticket.p, hout);
     after_launch("k_mgs");
 }
@@ -277,6 +280,7 @@ void multi_dot(Reducer& R, const double* const* dV, int k, const double* w, int6
     const int groups = (k + kGroup - 1) / kGroup;
     R.ensure(groups * kGroup, s);
     dim3 grid(reduce_blocks(n), groups);
+    acct_vec("k_multi_dot", 8.0 * n * (k + 1));
     k_multi_dot<<<grid, kRT, 0, s>>>(dV, k, w, n, R.partials.p, R.ticket.p, corr);
     after_launch("k_multi_dot");
 }
@@ -291,6 +295,7 @@ void reorth_apply(Reducer& R, double* w, const double* const* dV, const double* 
                   double* sc, cudaStream_t s)
 {
     R.ensure(1, s);
+    acct_vec("k_reorth_apply", 8.0 * n * (k + 2));
     k_reorth_apply<<<reduce_blocks(n), kRT, 0, s>>>(w, dV, corr, k, n, sc, R.partials.p, R.ticket.p);
     after_launch("k_reorth_apply");
 }
@@ -298,6 +303,7 @@ void reorth_apply(Reducer& R, double* w, const double* const* dV, const double* 
 void multi_axpy(double* x, const double* const* dV, const double* y, int k, int64_t n, cudaStream_t s)
 {
     if (n == 0 || k == 0) return;
+    acct_vec("k_multi_axpy", 8.0 * n * (k + 2));
     k_multi_axpy<<<ew_grid(n), 256, 0, s>>>(x, dV, y, k, n);
     after_launch("k_multi_axpy");
 }
@@ -305,6 +311,7 @@ void multi_axpy(double* x, const double* const* dV, const double* y, int k, int6
 void vec_fill(double* x, double v, int64_t n, cudaStream_t s)
 {
     if (n == 0) return;
+    acct_vec("k_fill", 8.0 * n);
     k_fill<<<ew_grid(n), 256, 0, s>>>(x, v, n);
     after_launch("k_fill");
 }
@@ -312,12 +319,14 @@ void vec_fill(double* x, double v, int64_t n, cudaStream_t s)
 void vec_copy(double* y, const double* x, int64_t n, cudaStream_t s)
 {
     if (n == 0 || y == x) return;
+    acct_vec("copy", 16.0 * n);
     ED_CUDA(cudaMemcpyAsync(y, x, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
 }
 
 void vec_sub_from(double* r, const double* b, int64_t n, cudaStream_t s)
 {
     if (n == 0) return;
+    acct_vec("k_sub_from", 24.0 * n);
     k_sub_from<<<ew_grid(n), 256, 0, s>>>(r, b, n);
     after_launch("k_sub_from");
 }
@@ -325,6 +334,7 @@ void vec_sub_from(double* r, const double* b, int64_t n, cudaStream_t s)
 void vec_mul(double* x, const double* w, int64_t n, cudaStream_t s)
 {
     if (n == 0) return;
+    acct_vec("k_mul", 24.0 * n);
     k_mul<<<ew_grid(n), 256, 0, s>>>(x, w, n);
     after_launch("k_mul");
 }
@@ -332,6 +342,7 @@ void vec_mul(double* x, const double* w, int64_t n, cudaStream_t s)
 void vec_add(double* x, const double* y, int64_t n, cudaStream_t s)
 {
     if (n == 0) return;
+    acct_vec("k_add", 24.0 * n);
     k_add<<<ew_grid(n), 256, 0, s>>>(x, y, n);
     after_launch("k_add");
 }
@@ -340,6 +351,7 @@ void vec_div_scalar(double* y, const double* x, const double* d, const double* g
                     cudaStream_t s)
 {
     if (n == 0) return;
+    acct_vec("k_div_scalar", 16.0 * n);
     k_div_scalar<<<ew_grid(n), 256, 0, s>>>(y, x, d, guard, n);
     after_launch("k_div_scalar");
 }
