@@ -335,27 +335,31 @@ __global__ void k_unique_write_warp(const int* __restrict__ keys, const int* __r
 // entries of B row K are split across lanes (distinct C columns inside one B
 // row), and __syncwarp orders consecutive K steps, so every C entry still
 // receives its products in csr_matmul's traversal order.
-constexpr int kWarpsPerCta = 8;  // kT / 32
-constexpr int kWarpCols = 1024;   // C row columns staged per warp (4 KB)
+constexpr int kNumWarpT = 128;   // threads per CTA of the warp-per-row numeric kernel
+constexpr int kNumWarps = kNumWarpT / 32;
+constexpr int kRowCache = 256;   // C row blocks accumulated in shared memory
 
 template <int RA, int KA, int CB>
-__global__ void k_spgemm_numeric_warp(const int* __restrict__ arp, const int* __restrict__ acol,
-                                      const double* __restrict__ aval, const int* __restrict__ brp,
-                                      const int* __restrict__ bcol, const double* __restrict__ bval,
-                                      const int* __restrict__ crp, const int* __restrict__ ccol, double* cval, int n)
+__global__ void __launch_bounds__(kNumWarpT) k_spgemm_numeric_warp(
+    const int* __restrict__ arp, const int* __restrict__ acol, const double* __restrict__ aval,
+    const int* __restrict__ brp, const int* __restrict__ bcol, const double* __restrict__ bval,
+    const int* __restrict__ crp, const int* __restrict__ ccol, double* cval, int n)
 {
-    // the C row's column list staged in shared memory (binary searches on
-    // shared instead of global memory) when it fits kWarpCols
-    __shared__ int s_cols[kWarpsPerCta][kWarpCols];
+    // rows of up to kRowCache blocks keep their column list and their
+    // accumulators (component c) in shared memory: the binary searches and the
+    // read-modify-writes stay on chip; the row is written out once at the end
+    __shared__ int s_cols[kNumWarps][kRowCache];
+    __shared__ double s_acc[kNumWarps][kRowCache * CB];
     const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int I = static_cast<int>(w / RA), c = static_cast<int>(w % RA);
     if (I >= n) return;
     const int c0 = crp[I], c1 = crp[I + 1], nc = c1 - c0;
-    const bool cached = nc <= kWarpCols;
+    const bool cached = nc <= kRowCache;
     const int* cc = cached ? s_cols[wib] : ccol + c0;
     if (cached) {
         for (int t = lane; t < nc; t += 32) s_cols[wib][t] = ccol[c0 + t];
+        for (int t = lane; t < nc * CB; t += 32) s_acc[wib][t] = 0.0; // C is zero-initialised
         __syncwarp();
     }
     for (int k = arp[I]; k < arp[I + 1]; ++k) {
@@ -369,7 +373,7 @@ __global__ void k_spgemm_numeric_warp(const int* __restrict__ arp, const int* __
                 if (cc[mid] < J) lo = mid + 1;
                 else hi = mid;
             }
-            double* cv = cval + static_cast<int64_t>(c0 + lo) * RA * CB + c * CB;
+            double* cv = cached ? s_acc[wib] + lo * CB : cval + static_cast<int64_t>(c0 + lo) * RA * CB + c * CB;
 #pragma unroll
             for (int d = 0; d < KA; ++d) {
                 const double a = aval[static_cast<int64_t>(k) * RA * KA + c * KA + d];
@@ -380,6 +384,9 @@ __global__ void k_spgemm_numeric_warp(const int* __restrict__ arp, const int* __
         }
         __syncwarp();
     }
+    if (cached)
+        for (int t = lane; t < nc * CB; t += 32)
+            cval[static_cast<int64_t>(c0 + t / CB) * RA * CB + c * CB + t % CB] = s_acc[wib][t];
 }
 
 // ---- csr_add (csr.cpp:168-198) on block rows -------------------------------
@@ -713,7 +720,7 @@ DBsr spgemm(const DBsr& A, const DBsr& B, cudaStream_t s)
     const bool wide_rows = tot_cand > 256LL * std::max(n, 1);
     if (A.Rb == 3 && A.Cb == 3 && B.Cb == 3) {
         if (wide_rows)
-            k_spgemm_numeric_warp<3, 3, 3><<<g1(32 * threads), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, B.rowptr.p,
+            k_spgemm_numeric_warp<3, 3, 3><<<static_cast<unsigned>((32 * threads + kNumWarpT - 1) / kNumWarpT), kNumWarpT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, B.rowptr.p,
                                                                           B.col.p, B.val.p, C.rowptr.p, C.col.p,
                                                                           C.val.p, n);
         else
@@ -721,7 +728,7 @@ DBsr spgemm(const DBsr& A, const DBsr& B, cudaStream_t s)
                                                                  B.val.p, C.rowptr.p, C.col.p, C.val.p, n);
     } else if (A.Rb == 1 && A.Cb == 1 && B.Cb == 1) {
         if (wide_rows)
-            k_spgemm_numeric_warp<1, 1, 1><<<g1(32 * threads), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, B.rowptr.p,
+            k_spgemm_numeric_warp<1, 1, 1><<<static_cast<unsigned>((32 * threads + kNumWarpT - 1) / kNumWarpT), kNumWarpT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, B.rowptr.p,
                                                                           B.col.p, B.val.p, C.rowptr.p, C.col.p,
                                                                           C.val.p, n);
         else
@@ -862,6 +869,12 @@ Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s)
         out.val = std::move(m.val);
         return out;
     }
+    return bsr_leveled(raw_of(m), s);
+}
+
+Bsr bsr_leveled(const DBsrRaw& m, cudaStream_t s)
+{
+    Bsr out;
     // level schedule needs the pattern on the host
     const double t_start = now_ms_host();
     BlockPattern pat;
@@ -875,10 +888,12 @@ Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s)
         std::fprintf(stderr, "[level-op] %-14s %8.2f ms\n", what, t - tl);
         tl = t;
     };
-    const std::vector<int> rp = m.rowptr.to_host(s);
-    pat.rowptr.assign(rp.begin(), rp.end());
-    pat.col = m.col.to_host(s);
+    std::vector<int> rp(static_cast<size_t>(m.nbr) + 1);
     pat.col.resize(m.nnzb);
+    ED_CUDA(cudaMemcpyAsync(rp.data(), m.rowptr, rp.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (m.nnzb) ED_CUDA(cudaMemcpyAsync(pat.col.data(), m.col, m.nnzb * sizeof(int), cudaMemcpyDeviceToHost, s));
+    ED_CUDA(cudaStreamSynchronize(s));
+    pat.rowptr.assign(rp.begin(), rp.end());
     lap("download");
     if (!pattern_symmetric(pat)) throw Error(ED_UNSUPPORTED, "Gauss-Seidel operator pattern is not symmetric");
     lap("symmetric");
@@ -902,14 +917,26 @@ Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s)
                      out.st->blocked ? out.st->ngroups : 0, now_ms_host() - t_start);
     const int E = m.Rb * m.Cb;
     out.val.alloc(std::max<int64_t>(m.nnzb * E, 1));
-    k_gather_rows<<<g1(m.nbr), kT, 0, s>>>(m.rowptr.p, m.val.p, out.st->perm.p ? out.st->perm.p : nullptr, m.nbr, E,
+    k_gather_rows<<<g1(m.nbr), kT, 0, s>>>(m.rowptr, m.val, out.st->perm.p ? out.st->perm.p : nullptr, m.nbr, E,
                                            out.st->rowptr.p, out.val.p);
     after_launch("k_gather_rows");
     ED_CUDA(cudaStreamSynchronize(s));
     return out;
 }
 
-DevSetupResult amg_build_device(const Bsr& A0, const AmgOpts& opts, cudaStream_t s)
+DevSetupResult amg_build_device_impl(const Bsr& A0, const AmgOpts& opts, cudaStream_t s, const LevelHook& on_level);
+
+DevSetupResult amg_build_device(const Bsr& A0, const AmgOpts& opts, cudaStream_t s, const LevelHook& on_level)
+{
+    try {
+        return amg_build_device_impl(A0, opts, s, on_level);
+    } catch (...) {
+        if (on_level) on_level(-1, DBsrRaw{});
+        throw;
+    }
+}
+
+DevSetupResult amg_build_device_impl(const Bsr& A0, const AmgOpts& opts, cudaStream_t s, const LevelHook& on_level)
 {
     const int k = opts.block_size;
     const int Bs = A0.st->Rb;
@@ -1059,6 +1086,7 @@ DevSetupResult amg_build_device(const Bsr& A0, const AmgOpts& opts, cudaStream_t
         res.levels.push_back(std::move(L));
         A = std::move(Ac);
         Bn = std::move(Bc);
+        if (on_level) on_level(lvl + 1, raw_of(A));
     }
     // coarsest level: dense COD on the host (amg.cpp:278-294)
     DevLevelData L;

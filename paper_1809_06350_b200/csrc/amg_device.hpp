@@ -15,6 +15,8 @@
 //   transpose       -- stable CUB radix sort by block column (csr.cpp:39-57)
 #pragma once
 
+#include <functional>
+
 #include "amg_host.hpp"
 #include "ed_internal.hpp"
 
@@ -27,6 +29,17 @@ struct DBsr {
     DevArray<int> rowptr, col;
     DevArray<double> val;
 };
+
+// Non-owning view of a natural-order device BSR (read by another host thread
+// while the owner moves the DBsr object itself; the device arrays stay put).
+struct DBsrRaw {
+    int nbr = 0, nbc = 0, Rb = 1, Cb = 1;
+    int64_t nnzb = 0;
+    const int* rowptr = nullptr;
+    const int* col = nullptr;
+    const double* val = nullptr;
+};
+inline DBsrRaw raw_of(const DBsr& m) { return DBsrRaw{m.nbr, m.nbc, m.Rb, m.Cb, m.nnzb, m.rowptr.p, m.col.p, m.val.p}; }
 
 struct DevLevelData {
     DBsr A, P, R;                 // P, R empty on the coarsest level
@@ -43,7 +56,11 @@ struct DevSetupResult {
 };
 
 // A0 given as a (possibly level-permuted) Bsr with block size == opts.block_size.
-DevSetupResult amg_build_device(const Bsr& A0, const AmgOpts& opts, cudaStream_t s);
+// on_level(l, A_l) is called on the building thread as soon as the Galerkin
+// operator of level l >= 1 is enqueued on s (its arrays stay valid until the
+// result is destroyed); on_level(-1, {}) before an exception leaves.
+using LevelHook = std::function<void(int, const DBsrRaw&)>;
+DevSetupResult amg_build_device(const Bsr& A0, const AmgOpts& opts, cudaStream_t s, const LevelHook& on_level = {});
 
 // One level of a collapsed coarse tail (dense_tail.cu): natural-order
 // operator, prolongator/restriction to the next level, inv_diag (device).
@@ -60,5 +77,7 @@ void dense_vcycle_operator(const std::vector<DenseTailLevel>& lv, const std::vec
 
 // Helpers shared with the V-cycle construction.
 Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s);
+// the leveled (Gauss-Seidel level-ordered) operator of m; reads m only
+Bsr bsr_leveled(const DBsrRaw& m, cudaStream_t s);
 
 } // namespace edb

@@ -246,7 +246,49 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
             ED_CUDA(cudaStreamSynchronize(s));
             std::fprintf(stderr, "[amg-build] %-22s %8.2f ms\n", what, now_ms() - t0);
         };
-        DevSetupResult R = amg_build_device(A0, o, s);
+        static const int tail_max = std::getenv("ED_DENSE_TAIL") ? std::atoi(std::getenv("ED_DENSE_TAIL")) : 4096;
+        const bool tails = o.smoother == 1 && tail_max > 0;
+        cudaStream_t ts = s == c.stream ? c.stream3 : c.stream4;
+        // The level-ordered operator of level 1 (host level schedule + ring
+        // layout, the longest host step of the setup) is built on its own host
+        // thread and stream while this thread builds the coarser levels.  Level
+        // 1 is never collapsed into the dense tail when it has > tail_max rows.
+        std::thread lop_th;
+        std::exception_ptr err_l;
+        Bsr pre_op;
+        int pre_l = -1;
+        struct Joiner {
+            std::thread& t;
+            ~Joiner()
+            {
+                if (t.joinable()) t.join();
+            }
+        } lop_joiner{lop_th};
+        auto on_level = [&](int l, const DBsrRaw& m) {
+            if (l < 0) {
+                if (lop_th.joinable()) lop_th.join();
+                return;
+            }
+            if (pre_l >= 0 || l != 1 || (tails && m.nbr * m.Rb <= tail_max) || std::getenv("ED_SERIAL_SETUP")) return;
+            pre_l = l;
+            cudaEvent_t ready;
+            ED_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+            ED_CUDA(cudaEventRecord(ready, s));
+            ED_CUDA(cudaStreamWaitEvent(ts, ready, 0));
+            ED_CUDA(cudaEventDestroy(ready));
+            lop_th = std::thread([&, m, ts] {
+                try {
+                    alloc_stream() = ts;
+                    ED_CUDA(cudaSetDevice(c.device));
+                    pre_op = bsr_leveled(m, ts);
+                    ED_CUDA(cudaStreamSynchronize(ts));
+                } catch (...) {
+                    err_l = std::current_exception();
+                }
+            });
+        };
+        DevSetupResult R = amg_build_device(A0, o, s, on_level);
+        Joiner lop_joiner_r{lop_th}; // joins before R (which the thread reads) is destroyed
         lap("device setup");
         setup_host_ms = 0.0;
         if (R.fallback) {
@@ -260,9 +302,8 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
         for (int l = 0; l < L; ++l) level_rows.push_back(R.levels[l].A.nbr * R.levels[l].A.Rb);
         // collapse the coarse tail: the first level below the fine one small
         // enough for a dense V-cycle operator (ED_DENSE_TAIL scalar rows, 0: off)
-        static const int tail_max = std::getenv("ED_DENSE_TAIL") ? std::atoi(std::getenv("ED_DENSE_TAIL")) : 4096;
         tail = -1;
-        if (o.smoother == 1 && tail_max > 0)
+        if (tails)
             for (int l = 1; l + 1 < L; ++l)
                 if (level_rows[l] <= tail_max) {
                     tail = l;
@@ -274,7 +315,6 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
         // level schedules); it reads only levels >= tail
         std::exception_ptr err_t;
         std::thread tail_th;
-        cudaStream_t ts = s == c.stream ? c.stream3 : c.stream4;
         if (tail >= 0) {
             cudaEvent_t ready;
             ED_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
@@ -296,13 +336,7 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
                 }
             });
         }
-        struct Joiner {
-            std::thread& t;
-            ~Joiner()
-            {
-                if (t.joinable()) t.join();
-            }
-        } joiner{tail_th};
+        Joiner joiner{tail_th};
         lv.resize(La);
         for (int l = 0; l < La; ++l) {
             DevLevel& d = lv[l];
@@ -315,6 +349,11 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
             }
             if (l == 0) {
                 d.A = &A0;
+            } else if (l == pre_l) {
+                lop_th.join();
+                if (err_l) std::rethrow_exception(err_l);
+                d.Aown = std::move(pre_op);
+                d.A = &d.Aown;
             } else {
                 d.Aown = bsr_from_dbsr(std::move(D.A), true, s);
                 d.A = &d.Aown;
