@@ -269,36 +269,46 @@ __device__ void build_frame(const AsmArgs& A, Frame& f, int e, int lane, bool ac
         f.tau = A.tau[e];
     }
     __syncthreads();
-    // --- B: kinematics + stress (Kinematics::from_F, evaluate_stress)
-    if (active && lane == 0) {
+    // --- B: kinematics + stress (Kinematics::from_F, evaluate_stress).  The
+    // three independent chains -- F^-1; C = F^T F and C^-1; J^-2/3 -- run on
+    // lanes 0, 1, 2 (each recomputes F and J identically), then lane 0 forms
+    // the stresses.
+    if (active && lane < 3) {
         double F[9] = {1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0};
         for (int a = 0; a < 4; ++a)
             for (int i = 0; i < 3; ++i)
                 for (int I = 0; I < 3; ++I) F[3 * i + I] = F[3 * i + I] + f.u[a][i] * f.G[a][I];
         const double J = det3(F);
         if (!(J > 0.0)) {
-            f.valid = 0;
-            atomicMin(A.bad_element, e);
-        } else {
+            if (lane == 0) {
+                f.valid = 0;
+                atomicMin(A.bad_element, e);
+            }
+        } else if (lane == 0) {
             f.valid = 1;
 #pragma unroll
             for (int k = 0; k < 9; ++k) f.F[k] = F[k];
             f.J = J;
             inv3(F, f.Finv);
+        } else if (lane == 1) {
             matTmul3(F, F, f.C);
             inv3(f.C, f.Cinv);
+        } else {
             f.Jm23 = pow(J, -2.0 / 3.0);
-#pragma unroll
-            for (int k = 0; k < 9; ++k) f.Ct[k] = f.C[k] * f.Jm23;
-            iso_stress(A.mat, f.Ct, f.St);
-            const double sc = ddot3(f.St, f.Ct);
-            const double c1 = -sc / 3.0;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) f.Siso[k] = f.St[k] * f.Jm23 + c1 * f.Cinv[k];
-            matmul3(f.F, f.Siso, f.Pt);
         }
     } else if (lane == 0) {
         f.valid = 0;
+    }
+    __syncthreads();
+    if (f.valid && lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) f.Ct[k] = f.C[k] * f.Jm23;
+        iso_stress(A.mat, f.Ct, f.St);
+        const double sc = ddot3(f.St, f.Ct);
+        const double c1 = -sc / 3.0;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) f.Siso[k] = f.St[k] * f.Jm23 + c1 * f.Cinv[k];
+        matmul3(f.F, f.Siso, f.Pt);
     }
     __syncthreads();
     if (!f.valid) return;
@@ -428,6 +438,10 @@ __global__ void __launch_bounds__(kCta, MINB) k_tangent(AsmArgs A, int c0, int c
     const bool active = idx < count;
     const int e = active ? A.elem_order[c0 + idx] : 0;
     Frame& f = frames[team];
+    // this lane's K4 block (128 B) is read-modified-written at the very end:
+    // start pulling its line into L1 now, behind the element's arithmetic
+    const int kslot = active ? A.k4slot[16 * static_cast<int64_t>(e) + lane] : 0;
+    if (active) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.k4 + 16 * static_cast<int64_t>(kslot)));
     build_frame(A, f, e, lane, active, true);
     if (!f.valid) return;
     if (lane < 12) ptilde_dir(A.mat, f, lane / 3, lane % 3, f.dP[lane]);
@@ -497,7 +511,7 @@ __global__ void __launch_bounds__(kCta, MINB) k_tangent(AsmArgs A, int c0, int c
         }
     }
     // scatter into K4 (fixed rows/columns are dropped later by the plane maps)
-    double* K = A.k4 + 16 * static_cast<int64_t>(A.k4slot[16 * static_cast<int64_t>(e) + lane]);
+    double* K = A.k4 + 16 * static_cast<int64_t>(kslot);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
 #pragma unroll
