@@ -14,6 +14,23 @@ namespace edb {
 
 namespace {
 
+// per-thread pinned staging buffer for the power iteration's D2H copies
+// (grown, never freed: a cudaFreeHost would synchronise the device under the
+// concurrent hierarchy builds)
+double* pinned_scratch(int n)
+{
+    thread_local double* p = nullptr;
+    thread_local int cap = 0;
+    if (n > cap) {
+        if (p) ED_CUDA(cudaFreeHost(p));
+        p = nullptr;
+        cap = std::max(n, 2 * cap);
+        ED_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p), sizeof(double) * cap));
+    }
+    return p;
+}
+
+
 constexpr int kT = 256;
 
 inline int g1(int64_t n) { return static_cast<int>(std::max<int64_t>(1, (n + kT - 1) / kT)); }
@@ -1039,29 +1056,44 @@ DevSetupResult amg_build_device_impl(const Bsr& A0, const AmgOpts& opts, cudaStr
         L.inv_diag = L.invd.to_host(s);
         double omega = 0.0;
         if (opts.smooth_prolongator) {
+            // power iteration (amg.cpp:170-185) with the reference's
+            // sequential norms on the host.  Only ||w|| gates the next launch;
+            // lambda = ||w|| / ||v|| is used after the last iteration only, so
+            // ||v|| is formed once, for the v that entered the last iteration
+            // (v = w_prev * (1/||w_prev||), bitwise the reference's update).
             DevArray<double> v(nrows), w(nrows);
             vec_fill(v.p, 1.0, nrows, s);
-            std::vector<double> hv(nrows, 1.0), hw(nrows);
-            double lambda = 1.0;
+            std::vector<double> hw(nrows), hw_prev;
+            double inv_prev = 0.0, lambda = 1.0;
             bool zero = false;
-            for (int it = 0; it < 10; ++it) {
+            int it = 0;
+            double* hbuf = pinned_scratch(nrows);
+            for (it = 0; it < 10; ++it) {
                 if (Bs == 3) k_spmv_seq<3, 3><<<g1(3LL * n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, v.p, w.p);
                 else k_spmv_seq<1, 1><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, v.p, w.p);
                 k_mul_vec<<<g1(nrows), kT, 0, s>>>(w.p, L.invd.p, nrows);
                 after_launch("k_spmv_seq");
-                w.download(hw.data(), s);
+                ED_CUDA(cudaMemcpyAsync(hbuf, w.p, sizeof(double) * nrows, cudaMemcpyDeviceToHost, s));
                 ED_CUDA(cudaStreamSynchronize(s));
+                if (it == 9) hw_prev.swap(hw); // w of iteration 8 (v of iteration 9 = hw_prev * inv_prev)
+                hw.assign(hbuf, hbuf + nrows);
                 const double nrm = amg_seq_norm(hw);
                 if (nrm == 0.0) {
                     lambda = 1.0;
                     zero = true;
                     break;
                 }
-                lambda = nrm / amg_seq_norm(hv);
                 const double inv = 1.0 / nrm;
-                for (int i = 0; i < nrows; ++i) hv[i] = hw[i] * inv;
-                k_scale_into<<<g1(nrows), kT, 0, s>>>(v.p, w.p, inv, nrows);
-                after_launch("k_scale_into");
+                if (it < 9) {
+                    k_scale_into<<<g1(nrows), kT, 0, s>>>(v.p, w.p, inv, nrows);
+                    after_launch("k_scale_into");
+                    inv_prev = inv;
+                } else {
+                    // v of this (last) iteration: all ones at it == 0, else w_prev / ||w_prev||
+                    std::vector<double> hv(nrows, 1.0);
+                    for (int i = 0; i < nrows; ++i) hv[i] = hw_prev[i] * inv_prev;
+                    lambda = nrm / amg_seq_norm(hv);
+                }
             }
             (void)zero;
             omega = 4.0 / (3.0 * std::max(lambda, 1e-12));
