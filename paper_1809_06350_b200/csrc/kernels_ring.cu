@@ -74,11 +74,14 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
         "{\n"
         ".reg .pred p;\n"
         "PW_%=:\n"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
         "@!p bra PW_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+    // one cluster-scope acquire after the spin (restricted to shared memory:
+    // the partials land in this CTA's shared memory), not one per poll
+    asm volatile("fence.acquire.sync_restrict::shared::cluster.cluster;" ::: "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 {
@@ -130,6 +133,12 @@ __global__ void __launch_bounds__(kT, 1) k_sgs_push(PushArgs q, const double* __
 {
     constexpr int BB = B * B;
     constexpr int PB = B == 3 ? 4 : 1; // doubles per partial entry (16-B aligned v2 pushes for B = 3)
+    // late partials by threads [0, kL), early sums by [kE0, kW).  Measured
+    // (ED_RING_PROF, A1 at 40^3): giving the two disjoint warp groups
+    // (kL = kE0 = 128) leaves the per-level time unchanged (~2,900 cycles
+    // profiled), so every worker does both in turn.
+    constexpr int kL = kW;
+    constexpr int kE0 = 0;
     extern __shared__ __align__(128) unsigned char dsm[];
     __shared__ __align__(8) uint64_t mbar[kNMB];
     __shared__ __align__(8) uint64_t pbar[kSlots];
@@ -254,26 +263,55 @@ __global__ void __launch_bounds__(kT, 1) k_sgs_push(PushArgs q, const double* __
     };
     // blocks [k0, k1) of a segment: acc += A_blocks z_cols (local z)
     auto seg_sum = [&](const View& v, int k0, int k1, int step, double* acc) {
-        for (int k = k0; k < k1; k += step) {
-            const double* zc = zs + v.pc[k];
-            const double* bl = v.pv + static_cast<int64_t>(k) * BB;
+        auto fma_blk = [&](const double* bl, const double* zz) {
+#pragma unroll
+            for (int d = 0; d < B; ++d)
+#pragma unroll
+                for (int r = 0; r < B; ++r) acc[r] = fma(bl[r * B + d], zz[d], acc[r]);
+        };
+        int k = k0;
+        // two blocks per trip: both blocks' column words, z and values are
+        // loaded before the FMAs (shared-memory latency overlapped), the FMAs
+        // keep the one-block-at-a-time order (results unchanged)
+        for (; k + step < k1; k += 2 * step) {
+            const int c0 = v.pc[k], c1 = v.pc[k + step];
+            double z0[B], z1[B], b0[BB], b1[BB];
 #pragma unroll
             for (int d = 0; d < B; ++d) {
-                const double zz = zc[d];
-#pragma unroll
-                for (int r = 0; r < B; ++r) acc[r] = fma(bl[r * B + d], zz, acc[r]);
+                z0[d] = zs[c0 + d];
+                z1[d] = zs[c1 + d];
             }
+            const double* p0 = v.pv + static_cast<int64_t>(k) * BB;
+            const double* p1 = v.pv + static_cast<int64_t>(k + step) * BB;
+#pragma unroll
+            for (int e = 0; e < BB; ++e) {
+                b0[e] = p0[e];
+                b1[e] = p1[e];
+            }
+            fma_blk(b0, z0);
+            fma_blk(b1, z1);
+        }
+        if (k < k1) {
+            const int c0 = v.pc[k];
+            double z0[B], b0[BB];
+#pragma unroll
+            for (int d = 0; d < B; ++d) z0[d] = zs[c0 + d];
+            const double* p0 = v.pv + static_cast<int64_t>(k) * BB;
+#pragma unroll
+            for (int e = 0; e < BB; ++e) b0[e] = p0[e];
+            fma_blk(b0, z0);
         }
     };
     // early phase of chunk v (workers only): each segment's early part
     // (columns not on the level solved just before it) by a group of G lanes,
     // reduced by shuffles in a fixed order -> es[j]
-    auto early = [&](const View& v, double* es) {
-        int lg = 5;
-        while (lg > 0 && (v.m << lg) > kW) --lg;
-        const int G = 1 << lg, lane = tid & (G - 1);
-        for (int j0 = 0; j0 < v.m; j0 += kW >> lg) {
-            const int j = j0 + (tid >> lg);
+    // t: thread index inside the early group of nt threads (whole warps)
+    auto early = [&](const View& v, double* es, int t, int nt) {
+        // largest lg <= 5 with m << lg <= nt (closed form, no per-thread loop)
+        const int lg = v.m > 0 ? min(5, max(0, 31 - __clz(nt / v.m))) : 5;
+        const int G = 1 << lg, lane = t & (G - 1);
+        for (int j0 = 0; j0 < v.m; j0 += nt >> lg) {
+            const int j = j0 + (t >> lg);
             double acc[B];
 #pragma unroll
             for (int r = 0; r < B; ++r) acc[r] = 0.0;
@@ -296,7 +334,7 @@ __global__ void __launch_bounds__(kT, 1) k_sgs_push(PushArgs q, const double* __
     };
 
     View cur = open_chunk(0);
-    if (tid < kW) early(cur, esum);
+    if (tid >= kE0 && tid < kW) early(cur, esum, tid - kE0, kW - kE0);
     __syncthreads();
     for (int li = 0; li < nlev; ++li) {
         const int par = li % kSlots;
@@ -308,8 +346,8 @@ __global__ void __launch_bounds__(kT, 1) k_sgs_push(PushArgs q, const double* __
         const double* es = esum + (li & 1) * q.maxm * B;
         // ---- early sum + late part (columns solved on the previous level,
         // fresh z), pushed to the owners
-        if (tid < kW) {
-            for (int j = tid; j < cur.m; j += kW) {
+        if (tid < kL) {
+            for (int j = tid; j < cur.m; j += kL) {
                 const int4 h = cur.segs[j];
                 const int na = h.w >> 16, nb = h.w & 0xFFFF;
                 double acc[B];
@@ -337,7 +375,8 @@ __global__ void __launch_bounds__(kT, 1) k_sgs_push(PushArgs q, const double* __
             if (tid < kW) {
                 nxt = open_chunk(li + 1);
                 if (prof) pt[5] += clock64() - t1;
-                if (!(PROF && (q.exp & 1))) early(nxt, esum + ((li + 1) & 1) * q.maxm * B);
+                if (tid >= kE0 && !(PROF && (q.exp & 1)))
+                    early(nxt, esum + ((li + 1) & 1) * q.maxm * B, tid - kE0, kW - kE0);
             }
         }
         const long long t2 = prof ? clock64() : 0;
@@ -345,6 +384,9 @@ __global__ void __launch_bounds__(kT, 1) k_sgs_push(PushArgs q, const double* __
         // a fixed tree, the diagonal block solved in sweep order
         if (tid >= kW) {
             const int lane = tid - kW;
+            // the next chunk's view while the partials travel (its copies were
+            // issued levels ago), not after the solve on the critical path
+            if (li + 1 < nlev) nxt = open_chunk(li + 1);
             const long long ta = prof7 ? clock64() : 0;
             long long tb = ta;
             for (int t = lane; t < cur.nown; t += 32) {
@@ -393,7 +435,6 @@ __global__ void __launch_bounds__(kT, 1) k_sgs_push(PushArgs q, const double* __
                 w7[0] += tb - ta;
                 w7[1] += tc - tb;
             }
-            if (li + 1 < nlev) nxt = open_chunk(li + 1);
         }
     const long long t3 = prof ? clock64() : 0;
         if (PROF && (rank == 0 || rank == 7) && li >= 200 && li < 264 && (tid & 31) == 0) {
