@@ -55,6 +55,7 @@ struct PushArgs {
     int nlev, cap, slice, part, maxm;
     long long* prof;
     int exp; // ED_PUSH_EXP (profiling builds only): 1 skip early sums, 2 skip late blocks
+    int lgmax; // log2 of the widest lane group per segment in the early sums
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(kT, 1) k_sgs_push(PushArgs q, const double* __
     // t: thread index inside the early group of nt threads (whole warps)
     auto early = [&](const View& v, double* es, int t, int nt) {
         // largest lg <= 5 with m << lg <= nt (closed form, no per-thread loop)
-        const int lg = v.m > 0 ? min(5, max(0, 31 - __clz(nt / v.m))) : 5;
+        const int lg = min(q.lgmax, v.m > 0 ? min(5, max(0, 31 - __clz(nt / v.m))) : 5);
         const int G = 1 << lg, lane = t & (G - 1);
         for (int j0 = 0; j0 < v.m; j0 += nt >> lg) {
             const int j = j0 + (t >> lg);
@@ -493,6 +494,16 @@ __global__ void k_ring_pack(const int* __restrict__ psrc, const int* __restrict_
     }
 }
 
+// widest lane group per segment of the early sums (log2): narrower groups mean
+// fewer shuffle rounds and fewer issuing warps per level.  Measured at 40^3
+// (ED_PUSH_LG sweep, profiles/r01d_ncu_summary.md): A1 sweep 674 us at 5, 661-665
+// at 3 and 2, 706 at 1; S0 430 us at 5, 427 at 2
+template <int B>
+constexpr int kLgMax()
+{
+    return B == 3 ? 3 : 2;
+}
+
 template <int B>
 void launch(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s,
             const double* packed)
@@ -513,7 +524,8 @@ void launch(const Bsr& A, const double* b, double* z, const double* invd, bool f
     const PushArgs q{S.rchunk.p, S.rseg.p,     S.rpcol.p, packed,     packed + ((S.ring_npk + 1) & ~1LL) * B * B,
                      S.rown.p,   S.rown_ptr.p, S.nlev(),  S.ring_cap, slice,
                      S.ring_part, S.ring_maxm, prof_on ? prof : nullptr,
-                     std::getenv("ED_PUSH_EXP") ? std::atoi(std::getenv("ED_PUSH_EXP")) : 0};
+                     std::getenv("ED_PUSH_EXP") ? std::atoi(std::getenv("ED_PUSH_EXP")) : 0,
+                     std::getenv("ED_PUSH_LG") ? std::atoi(std::getenv("ED_PUSH_LG")) : kLgMax<B>()};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(S.ring_cs, 1, 1);
     cfg.blockDim = dim3(kT, 1, 1);
