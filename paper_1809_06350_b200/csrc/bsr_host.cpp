@@ -481,7 +481,8 @@ std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLay
     const int n = pat.nbr;
     S.L = lanes > 0 ? lanes : auto_lanes(n > 0 ? static_cast<double>(S.nnzb) / n : 1.0, Rb * Cb);
     // sweeps are latency-bound: as many lanes as blocks per row (shorter chains)
-    S.Ls = lanes > 0 ? lanes : auto_lanes(n > 0 ? static_cast<double>(S.nnzb) / n : 1.0, 9);
+    static const int ls_env = std::getenv("ED_SGS_LANES") ? std::atoi(std::getenv("ED_SGS_LANES")) : 0;
+    S.Ls = lanes > 0 ? lanes : ls_env > 0 ? ls_env : auto_lanes(n > 0 ? static_cast<double>(S.nnzb) / n : 1.0, 9);
     S.h_rowptr.assign(n + 1, 0);
     S.h_col.assign(S.nnzb, 0);
     bool identity = true;
