@@ -1129,6 +1129,7 @@ DevSetupResult amg_build_device_impl(const Bsr& A0, const AmgOpts& opts, cudaStr
     else k_invdiag<1><<<g1(n), kT, 0, s>>>(A.rowptr.p, A.col.p, A.val.p, n, L.invd.p);
     after_launch("k_invdiag");
     L.inv_diag = L.invd.to_host(s);
+    check_coarse_size(nr, static_cast<int>(res.levels.size()));
     const HostCsr Ah = to_host_csr(A, s);
     std::vector<double> dense(static_cast<size_t>(nr) * nr, 0.0);
     for (int r = 0; r < nr; ++r)

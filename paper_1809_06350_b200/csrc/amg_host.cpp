@@ -569,6 +569,21 @@ HostCsr amg_tentative(int nrows, int k, const std::vector<int>& agg_of_row, int 
 
 double amg_seq_norm(const std::vector<double>& v) { return seq_norm(v); }
 
+void check_coarse_size(int nrows, int n_coarsened)
+{
+    // The reference factors the coarsest level densely whatever its size
+    // (amg.cpp:278-294).  When coarsening stalls before coarse_max_rows the
+    // loop stops at max_levels with a huge coarsest level; a dense COD of it
+    // cannot be formed (the reference would die in the same place), so say so.
+    if (nrows <= kMaxCoarseDenseRows) return;
+    char msg[256];
+    std::snprintf(msg, sizeof msg,
+                  "amg: coarsest level has %d rows after %d coarsening steps (coarsening stalled); its dense "
+                  "COD (amg.cpp:286-294) would need %.1f GB",
+                  nrows, n_coarsened, 8.0 * double(nrows) * double(nrows) / 1e9);
+    throw Error(ED_UNSUPPORTED, msg);
+}
+
 std::vector<double> cod_pinv(const std::vector<double>& dense_colmajor, int n, double threshold)
 {
     Cod cod;
@@ -689,6 +704,7 @@ HostHierarchy amg_build_host(const HostCsr& A0, const AmgOpts& opts)
         h.levels.push_back(std::move(lv));
     }
     const HostCsr& Ac = h.levels.back().A;
+    check_coarse_size(Ac.nrows, static_cast<int>(h.levels.size()) - 1);
     h.nc = Ac.nrows;
     std::vector<double> dense(static_cast<size_t>(Ac.nrows) * Ac.ncols, 0.0);
     for (int r = 0; r < Ac.nrows; ++r)

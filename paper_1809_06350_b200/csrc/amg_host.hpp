@@ -56,6 +56,9 @@ std::vector<double> csr_diag(const HostCsr& a);
 
 // Complete orthogonal decomposition pseudo-inverse (min-norm LS solve
 // operator) with the rank threshold of Eigen's COD.setThreshold(t).
+// Largest coarsest level whose dense COD is formed (16384^2 doubles = 2 GB).
+constexpr int kMaxCoarseDenseRows = 16384;
+void check_coarse_size(int nrows, int n_coarsened);
 std::vector<double> cod_pinv(const std::vector<double>& dense_colmajor, int n, double threshold);
 
 } // namespace edb

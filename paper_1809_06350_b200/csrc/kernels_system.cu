@@ -113,28 +113,32 @@ __global__ void __launch_bounds__(kRT) k_shat(ShatArgs a)
 
 __global__ void k_predict_blend(NewtonArgs a)
 {
+    // The yn_* and cur_* slots may alias (ed_newton_first_pass predicts in
+    // place), so every y_n value is read into a register before any store.
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t n3 = 3 * static_cast<int64_t>(a.n_nodes);
     if (i < n3) {
+        const double ud = a.yn_udot[i], vd = a.yn_vdot[i], u = a.yn_u[i], v = a.yn_v[i];
         // predictor: rates scaled by (gamma-1)/gamma (timeint.cpp:57-61)
-        const double cud = a.yn_udot[i] * a.pf;
-        const double cvd = a.yn_vdot[i] * a.pf;
+        const double cud = ud * a.pf;
+        const double cvd = vd * a.pf;
         a.cur_udot[i] = cud;
         a.cur_vdot[i] = cvd;
-        a.cur_u[i] = a.yn_u[i];
-        a.cur_v[i] = a.yn_v[i];
+        a.cur_u[i] = u;
+        a.cur_v[i] = v;
         // blends (timeint.cpp:88-93, blend at :31-36)
-        a.mid_udot[i] = a.yn_udot[i] + a.alpha_m * (cud - a.yn_udot[i]);
-        a.mid_vdot[i] = a.yn_vdot[i] + a.alpha_m * (cvd - a.yn_vdot[i]);
-        a.mid_u[i] = a.yn_u[i] + a.alpha_f * (a.yn_u[i] - a.yn_u[i]);
-        a.mid_v[i] = a.yn_v[i] + a.alpha_f * (a.yn_v[i] - a.yn_v[i]);
+        a.mid_udot[i] = ud + a.alpha_m * (cud - ud);
+        a.mid_vdot[i] = vd + a.alpha_m * (cvd - vd);
+        a.mid_u[i] = u + a.alpha_f * (u - u);
+        a.mid_v[i] = v + a.alpha_f * (v - v);
     }
     if (i < a.n_nodes) {
-        const double cpd = a.yn_pdot[i] * a.pf;
+        const double pd = a.yn_pdot[i], p = a.yn_p[i];
+        const double cpd = pd * a.pf;
         a.cur_pdot[i] = cpd;
-        a.cur_p[i] = a.yn_p[i];
-        a.mid_pdot[i] = a.yn_pdot[i] + a.alpha_m * (cpd - a.yn_pdot[i]);
-        a.mid_p[i] = a.yn_p[i] + a.alpha_f * (a.yn_p[i] - a.yn_p[i]);
+        a.cur_p[i] = p;
+        a.mid_pdot[i] = pd + a.alpha_m * (cpd - pd);
+        a.mid_p[i] = p + a.alpha_f * (p - p);
     }
 }
 

@@ -24,3 +24,23 @@ def oracle():
     from oracle import ref
     ref.lib()
     return ref
+
+
+_PARITY = []
+
+
+@pytest.fixture(scope="session")
+def parity_log():
+    """Collects per-case parity figures (counts, max history deviation, x error);
+    written as JSON to $PARITY_LOG at the end of the session (committed under
+    profiles/ as the evidence behind the GPU parity claims)."""
+    return _PARITY
+
+
+def pytest_sessionfinish(session, exitstatus):
+    path = os.environ.get("PARITY_LOG")
+    if path and _PARITY:
+        import json
+        os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+        with open(path, "w") as f:
+            json.dump(_PARITY, f, indent=1, default=float)
