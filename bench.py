@@ -56,9 +56,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (profiling runs)")
     ap.add_argument("--spmv-n", type=int, default=160,
-                    help="cube size of the standalone SpMV leg (the metric's 160^3 BSR SpMV GB/s); 0 skips it")
-    ap.add_argument("--ref-budget-s", type=float, default=240.0,
-                    help="reference arm: wall budget of the timed steps; beyond it each step is a smaller cube")
+                    help="cube size of the 160^3 leg (the metric's BSR SpMV GB/s, assembly, Newton pass); 0 skips it")
+    ap.add_argument("--big-dt", type=float, default=1e-2, help="time step of the 160^3 leg")
+    ap.add_argument("--big-newton", type=int, default=1, help="time one whole first Newton pass at 160^3 (0: skip)")
     a = ap.parse_args()
     cfg = {0: (10, 0.4, 1e-3), 1: (40, 0.5, 1e-3), 2: (100, 0.45, 0.1), 4: (160, 0.5, 0.1)}[a.config]
     a.n = a.n or cfg[0]
@@ -170,67 +170,118 @@ def cpu_reference_step(n, nu, dt):
     return time.perf_counter() - t0, out, cp
 
 
+def _ref_worker(a):
+    n, nu, dt = a
+    t, out, cp = cpu_reference_step(n, nu, dt)
+    return t, out["stats"], cp.nv + cp.np
+
+
+def _host_mem_gb():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) / 1e6
+    except OSError:
+        pass
+    return 16.0
+
+
 def run_reference(args, world, rank, dist):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    reference compiled from its sources) on the SAME workload as our arm:
+    K full first corrector passes of the seeded configs[i] cube.  The
+    reference is single-threaded, so the host's cores run K independent
+    passes as replicas (one process each, at most one per core and as many
+    as host memory allows); value = K / wall time of the timed set."""
     if rank != 0:
         return
-    n = args.cpu_sample_n
-    # the reference has no warm-up effects (no JIT, no caches across solves):
-    # warm the process once on a tiny cube instead of W full samples
-    if args.warmup > 0:
-        cpu_reference_step(4, args.nu, args.dt)
-    # bounded: one full first pass on the workload cube is ~36 s single-threaded;
-    # when K of them would exceed the budget, each step is a smaller seeded cube
-    # and the rate is normalised per unknown to the workload (said in `sample`)
-    t1, _, _ = cpu_reference_step(n, args.nu, args.dt) if args.steps * 36.0 > args.ref_budget_s else (None, None, None)
-    n_s = n
-    if t1 is not None:
-        per_step = args.ref_budget_s / args.steps
-        while n_s > 8 and t1 * (n_s / n) ** 3 > per_step:
-            n_s -= 4
-    times = []
-    for _ in range(args.steps):
-        t, out, cp = cpu_reference_step(n_s, args.nu, args.dt)
-        times.append(t)
-    tot = sum(times)
+    import concurrent.futures as cf
+    import multiprocessing as mp
+
     from paper_1809_06350_b200 import CubeProblem
+
     cw = CubeProblem(n=args.n, nu=args.nu, dt=args.dt)
-    scale = (cp.nv + cp.np) / (cw.nv + cw.np)  # solves/s of the sample -> of the workload, per unknown
-    value = args.steps / tot * scale
-    sample = (f"reference (oracle/_ref, 1 thread) first corrector pass on the {n_s}^3 cube ({cp.nv + cp.np} unknowns, "
-              f"seeded, nu={args.nu}, dt={args.dt})"
-              + ("" if n_s == args.n else f"; bounded sample of the {args.n}^3 workload, rate scaled by unknowns ({scale:.4f})"))
+    unknowns = cw.nv + cw.np
+    gb_per_pass = 0.5 + 13.5e-6 * unknowns  # measured peak RSS: 3.6 GB for the 40^3 pass
+    cores = os.cpu_count() or 1
+    procs = max(1, min(cores, args.steps, int(_host_mem_gb() * 0.8 / gb_per_pass)))
+    ctx = mp.get_context("fork")
+    with cf.ProcessPoolExecutor(max_workers=procs, mp_context=ctx) as ex:
+        if args.warmup > 0:  # no JIT or caches to warm: one tiny cube per worker
+            list(ex.map(_ref_worker, [(4, args.nu, args.dt)] * procs))
+        t0 = time.perf_counter()
+        res = list(ex.map(_ref_worker, [(args.n, args.nu, args.dt)] * args.steps))
+        wall = time.perf_counter() - t0
+    value = args.steps / wall
+    per_pass = [r[0] for r in res]
+    sample = (f"reference (oracle/_ref, the unmodified reference compiled from its sources) first corrector pass on "
+              f"the {args.n}^3 cube ({unknowns} unknowns, seeded, nu={args.nu}, dt={args.dt}), {args.steps} passes "
+              f"as {procs} concurrent single-threaded processes; mean single-pass time {statistics.mean(per_pass):.2f} s")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64 state)",
-        "config": {"workload": f"configs[{args.config}]: cube {args.n}^3 first Newton corrector pass", "n": n,
-                   "nu": args.nu, "dt": args.dt},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference", "sample": sample},
+        "config": workload_config(args, cw),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "reference", "sample": sample,
+                         "single_pass_s": per_pass, "stats": res[-1][1]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
-def spmv_leg(n, device, peak):
-    """The metric's BSR SpMV GB/s at the 160^3 cube (configs[4] size, 16.6 M
-    unknowns, ~9 GB coupled matrix >> 126 MB L2): mesh + residual + tangent
-    assembly on the device, then the coupled / A-plane / S_hat SpMVs and the fine
-    Gauss-Seidel half sweep, each timed with CUDA events over 5 launches."""
+def workload_config(args, cp):
+    return {"workload": f"configs[{args.config}]: cube {args.n}^3 first Newton corrector pass", "n": args.n,
+            "nu": args.nu, "dt": args.dt, "unknowns": cp.nv + cp.np, "tets": cp.mesh.n_tets,
+            "solver": "FGMRES(200) 1e-6 / SCR a,s,inner 1e-2, AMG SGS (reference defaults)"}
+
+
+def cube_leg(n, dt, device, peak, newton):
+    """The metric's 160^3 quantities (configs[4] size: 16.6 M unknowns, ~9 GB
+    coupled matrix >> 126 MB L2).  Mesh, residual and tangent assembly on the
+    device; the coupled / A-plane / S_hat SpMVs and the fine Gauss-Seidel half
+    sweep, each timed with CUDA events over 5 launches; assembly rates; and,
+    when `newton`, one whole first Newton corrector pass (both AMG setups and
+    the nested FGMRES solve; a warm-up pass first builds the mesh-static
+    structures), device-timed, with its counts and phase split."""
     import gc
 
     from paper_1809_06350_b200 import CubeProblem
 
     t0 = time.perf_counter()
-    cp = CubeProblem(n=n, nu=0.5, dt=0.1)
+    cp = CubeProblem(n=n, nu=0.5, dt=dt)
+    st = cp.seeded_state()
     ctx = cp.context(device)
-    ctx.set_state(cp.seeded_state())
+    ctx.set_state(st)
     ctx.assemble_residuals()
     ctx.assemble_tangent(cp.ts)
     k = ctx.bench_kernels(cp.solver_options(), n_rep=5)
-    out = {"n": n, "unknowns": cp.nv + cp.np, "tets": cp.mesh.n_tets, "setup_s": round(time.perf_counter() - t0, 1)}
+    out = {"n": n, "dt": dt, "nu": 0.5, "unknowns": cp.nv + cp.np, "tets": cp.mesh.n_tets,
+           "setup_s": round(time.perf_counter() - t0, 1)}
+    spmv = {}
     for name, (ms, by) in k.items():
         gbs = by / (ms * 1e-3) / 1e9
-        out[name] = {"ms": ms, "bytes": by, "achieved_gbs": gbs, "frac": gbs / peak}
+        spmv[name] = {"ms": ms, "bytes": by, "achieved_gbs": gbs, "frac": gbs / peak, "frac_8tbs": gbs / 8000.0}
+    out["spmv"] = spmv
     out["assembly"] = assembly_row(ctx.bench_assembly(cp.ts, n_rep=3), peak)
+    if newton:
+        opts = cp.solver_options()
+        ctx.set_state(st)
+        ctx.state_save()
+        passes = []
+        for rep in range(2):
+            ctx.state_restore()
+            ctx.timer_start()
+            o = ctx.newton_first_pass(cp.ts, opts)
+            ms = ctx.timer_stop()
+            passes.append({"ms": ms, "stats": o["stats"], "norm": o["norm"], "history": [float(h) for h in o["history"]],
+                           "phase_ms": o["times"]})
+        last = passes[-1]
+        out["newton"] = {"solves_per_s": 1e3 / last["ms"], "pass_ms": last["ms"], "warm_pass_ms": passes[0]["ms"],
+                         "stats": last["stats"], "norm": last["norm"], "history": last["history"],
+                         "phase_ms": last["phase_ms"],
+                         "note": "device-timed first corrector pass (residual, tangent, both AMG setups, nested "
+                                 "FGMRES, update) from the seeded state; the reference cannot run this size "
+                                 "(DESIGN.md §5), so there is no same-config CPU number"}
     ctx.close()
     del ctx, cp
     gc.collect()
@@ -392,16 +443,13 @@ def run_ours(args, world, rank, local, dist):
                "sample": f"reference (oracle/_ref, 1 thread) first corrector pass on the {args.cpu_sample_n}^3 cube "
                          f"({cpc.nv + cpc.np} unknowns) in {t_cpu:.2f} s"
                          + ("" if args.cpu_sample_n == args.n else f" (bounded sample of the {args.n}^3 workload)")}
-    spmv = spmv_leg(args.spmv_n, local, peak) if args.spmv_n > 0 else None
+    big = cube_leg(args.spmv_n, args.big_dt, local, peak, args.big_newton) if args.spmv_n > 0 else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64 state, SURVEY.md §8d)",
-        "config": {"workload": f"configs[{args.config}]: cube {args.n}^3 first Newton corrector pass", "n": args.n,
-                   "nu": args.nu, "dt": args.dt, "unknowns": cp.nv + cp.np, "tets": cp.mesh.n_tets,
-                   "parallelism": f"replicas{world}",
-                   "l2_flush": "none needed for the step (AMG setup rewrites every level each step); kernel rows: cold inputs",
-                   "solver": "FGMRES(200) 1e-6 / SCR a,s,inner 1e-2, AMG SGS (reference defaults)"},
+        "config": dict(workload_config(args, cp), parallelism=f"replicas{world}",
+                       l2_flush="none needed for the step (AMG setup rewrites every level each step); kernel rows: cold inputs"),
         "roofline": {"bound": "hbm", "kernel": top, "achieved": head["achieved_gbs"], "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": head["achieved_gbs"] / peak,
                      "traffic": traffic,
@@ -409,7 +457,7 @@ def run_ours(args, world, rank, local, dist):
                               "dependency levels x per-level latency, not bytes (DESIGN.md §4)"),
                      "live_kernels": dict(list(live.items())[:10]), "standalone_kernels": micro,
                      "solve": solve_roof},
-        "spmv_cfg4": spmv,
+        "cfg4": big,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms": e2e_ms, "host_inputs": "pinned", "phase_ms_last": e2e_phase},

@@ -64,7 +64,7 @@ typedef struct {
 
 /* BlockSolverOptions, precond.hpp:167-175 (PrecondKind order, :159-165) */
 typedef struct {
-    int32_t precond; /* 0 nested (only kind built here; others -> ED_UNSUPPORTED) */
+    int32_t precond; /* PrecondKind: 0 Nested, 1 Simple, 2 Ilu0, 3 Jacobi, 4 None (all built) */
     int32_t scale;
     ed_krylov_config outer, a, s, inner; /* outer; ScrTolerances a/s/inner (precond.hpp:83-87) */
     ed_amg_options amg_a, amg_s;
@@ -124,11 +124,6 @@ int64_t ed_kernel_launches(const ed_ctx* ctx);      /* launches issued so far by
  * mesh.cpp:94-103); grad_n: 12 per element [a][I]; volume, tau per element. */
 int ed_mesh_upload(ed_ctx* ctx, int n_nodes, int n_tets, const int32_t* tets,
                    const double* grad_n, const double* volume, const double* tau);
-/* Optional node coordinates (Mesh::nodes, mesh.hpp:24-50), 3 doubles per
- * node.  Not used by any arithmetic: they let the fine Gauss-Seidel level be
- * partitioned into spatial tiles for the tiled cluster sweep.  Call before
- * ed_dofs_build. */
-int ed_mesh_coords(ed_ctx* ctx, int n_nodes, const double* xyz);
 /* fixed: 3 bytes per node (DofMap::build, assembly.cpp:11-27).  Nodes must be
  * fully free or fully fixed (else ED_UNSUPPORTED).  Returns nv, np. */
 int ed_dofs_build(ed_ctx* ctx, const uint8_t* fixed, int32_t* nv, int32_t* np);

@@ -22,7 +22,7 @@ ED_CUDA_ERROR, ED_NOT_READY, ED_UNSUPPORTED = 4, 5, 6
 
 EXPORTED = [
     "ed_ctx_create", "ed_ctx_destroy", "ed_last_error", "ed_ctx_set_threads", "ed_kernel_launches",
-    "ed_mesh_upload", "ed_mesh_coords", "ed_dofs_build", "ed_set_material", "ed_set_loads", "ed_state_upload",
+    "ed_mesh_upload", "ed_dofs_build", "ed_set_material", "ed_set_loads", "ed_state_upload",
     "ed_state_download", "ed_assemble_residuals", "ed_assemble_tangent", "ed_tangent_export",
     "ed_foldin_download", "ed_block_system_upload", "ed_solve_block_system",
     "ed_solve_block_system_device", "ed_newton_first_pass", "ed_step_generalized_alpha", "ed_block_matvec", "ed_gmres_a",
@@ -125,7 +125,6 @@ def lib():
         "ed_ctx_set_threads": (C.c_int, [P, C.c_int]),
         "ed_kernel_launches": (_i64, [P]),
         "ed_mesh_upload": (C.c_int, [P, C.c_int, C.c_int, ip, dp, dp, dp]),
-        "ed_mesh_coords": (C.c_int, [P, C.c_int, dp]),
         "ed_dofs_build": (C.c_int, [P, u8p, ip, ip]),
         "ed_set_material": (C.c_int, [P, C.POINTER(Material)]),
         "ed_set_loads": (C.c_int, [P, dp, C.c_int, ip, dp, dp]),

@@ -209,8 +209,6 @@ class Context:
         self._chk(N.lib().ed_mesh_upload(self._p, mesh.n_nodes, mesh.n_tets, N.ip(N.i32(mesh.tets.ravel())),
                                          N.dp(N.f64(mesh.grad_n.ravel())), N.dp(N.f64(mesh.volume)),
                                          N.dp(N.f64(tau))))
-        # coordinates only steer the sweep partition (tiled fine-level Gauss-Seidel)
-        self._chk(N.lib().ed_mesh_coords(self._p, mesh.n_nodes, N.dp(N.f64(mesh.nodes.ravel()))))
 
     def build_dofs(self, fixed: np.ndarray):
         """DofMap::build (assembly.cpp:11-27); fixed is (N, 3) bool."""

@@ -415,6 +415,9 @@ int guarded(ed_ctx* h, F&& f)
         ~StreamScope() { alloc_stream() = prev; }
     } scope(h->c.stream);
     try {
+        // every entry point runs on the context's device (several contexts on
+        // different GPUs may share one host thread)
+        ED_CUDA(cudaSetDevice(h->c.device));
         f(h->c);
         h->c.err.clear();
         return ED_OK;
@@ -482,16 +485,6 @@ int ed_mesh_upload(ed_ctx* ctx, int n_nodes, int n_tets, const int32_t* tets, co
         c.sync();
         c.have_mesh = true;
         c.have_dofs = false;
-        c.sys_from_mesh = false;
-    });
-}
-
-int ed_mesh_coords(ed_ctx* ctx, int n_nodes, const double* xyz)
-{
-    return guarded(ctx, [&](Ctx& c) {
-        check(xyz != nullptr && n_nodes > 0, ED_INVALID_ARGUMENT, "bad coordinates");
-        c.h_xyz.assign(xyz, xyz + 3LL * n_nodes);
-        c.have_dofs = false; // the velocity layout (sweep partition) is rebuilt with them
         c.sys_from_mesh = false;
     });
 }
@@ -1218,7 +1211,7 @@ int ed_bench_kernels(ed_ctx* ctx, const ed_block_solver_options* opts, int n_rep
         out[2] = time([&] { spmv(W.A, x.p, y.p, nullptr, 0, c.stream); });
         out[3] = W.A.bytes_per_spmv();
         DevArray<double> gd;
-        blocked_dense(W.A, gd, c.stream);
+        sweep_prepare(W.A, invd.p, gd, c.stream);
         out[4] = time([&] { sgs_sweep(W.A, x.p, y.p, invd.p, true, c.stream, gd.p); });
         // values+indices once, plus b and inv_diag read, z read+written
         out[5] = W.A.st->nnzb * (8.0 * W.Bv * W.Bv + 4.0) + 4.0 * (W.A.st->nbr + 1) + 4.0 * 8.0 * nv;

@@ -162,152 +162,6 @@ int ring_order(const BlockPattern& pat, int B, std::vector<int>& order, const st
     return cs;
 }
 
-// ---- tiled cluster sweep (kernels_tile.cu) --------------------------------
-namespace {
-constexpr int kTileSliceMaxBytes = 112 * 1024; // z slice per CTA
-constexpr int kTileMinRows = 4096;
-
-int tile_entry_bytes(int64_t m, int64_t kb, int64_t ke, int B)
-{
-    const int64_t cb = 4 * (((ke + 3) & ~int64_t(3)) - (kb & ~int64_t(3)));
-    const int64_t vb = 8LL * B * B * (((ke + 1) & ~int64_t(1)) - (kb & ~int64_t(1)));
-    return static_cast<int>(16 * m + cb + vb);
-}
-} // namespace
-
-int tile_order(const BlockPattern& pat, int B, const std::vector<double>& xyz, std::vector<int>& order,
-               const std::vector<int>& level_of_pos, int nlev, std::vector<int>& owner)
-{
-    // opt-in (ED_TILE=1): measured 0.67 ms per 40^3 fine half sweep against
-    // 0.275 ms for the dataflow kernel -- each level's rows (up to ~75 per CTA,
-    // 15 blocks each) exceed one ring entry and b / inv_diag come from global
-    // memory on the critical path
-    static const bool on = std::getenv("ED_TILE") != nullptr;
-    const int n = pat.nbr;
-    if (!on || (B != 1 && B != 3) || nlev < 2 || n < kTileMinRows || pat.nbr != pat.nbc ||
-        static_cast<int64_t>(xyz.size()) != 3LL * n)
-        return 0;
-    const int cs = ring_cluster_size();
-    if (cs != 16 && cs != 8) return 0;
-    const int nx = 4, ny = cs / 4;
-    // equal-count bisection: x into nx slabs, each slab by y into ny tiles
-    std::vector<int> idx(n);
-    std::iota(idx.begin(), idx.end(), 0);
-    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return xyz[3 * a] < xyz[3 * b]; });
-    owner.assign(n, 0);
-    for (int gx = 0; gx < nx; ++gx) {
-        const int a = static_cast<int>(static_cast<int64_t>(n) * gx / nx), b = static_cast<int>(static_cast<int64_t>(n) * (gx + 1) / nx);
-        std::stable_sort(idx.begin() + a, idx.begin() + b, [&](int p, int q) { return xyz[3 * p + 1] < xyz[3 * q + 1]; });
-        for (int gy = 0; gy < ny; ++gy) {
-            const int c0 = a + static_cast<int>(static_cast<int64_t>(b - a) * gy / ny);
-            const int c1 = a + static_cast<int>(static_cast<int64_t>(b - a) * (gy + 1) / ny);
-            for (int t = c0; t < c1; ++t) owner[idx[t]] = gx * ny + gy;
-        }
-    }
-    std::vector<int64_t> slice(cs, 0);
-    for (int r = 0; r < n; ++r) ++slice[owner[r]];
-    const int64_t smax = *std::max_element(slice.begin(), slice.end());
-    if (smax * B * 8 > kTileSliceMaxBytes) return 0;
-    const int cap = tile_capacity(static_cast<int>(smax * B));
-    // a single row must fit a third of the ring (sub-chunks split levels by rows)
-    for (int r = 0; r < n; ++r)
-        if (3 * tile_entry_bytes(1, 0, pat.rowptr[r + 1] - pat.rowptr[r] + 1, B) > cap) return 0;
-    // CTA-major inside every level, stable in the level order
-    std::vector<int> neworder;
-    neworder.reserve(n);
-    int a = 0;
-    while (a < n) {
-        int b = a;
-        while (b < n && level_of_pos[b] == level_of_pos[a]) ++b;
-        for (int c = 0; c < cs; ++c)
-            for (int p = a; p < b; ++p)
-                if (owner[order[p]] == c) neworder.push_back(order[p]);
-        a = b;
-    }
-    order.swap(neworder);
-    return cs;
-}
-
-static void tile_build(BsrStruct& S, const BsrLayout& lay, cudaStream_t s)
-{
-    const int cs = lay.tile_cs, n = S.nbr, nlev = S.nlev(), B = S.Rb;
-    std::vector<int> cnt(cs, 0), local(n), own_ptr(cs + 1, 0), stored_owner(n);
-    std::vector<std::vector<int>> own(cs);
-    for (int q = 0; q < n; ++q) {
-        const int c = lay.tile_owner[lay.perm[q]];
-        stored_owner[q] = c;
-        local[q] = cnt[c]++;
-        own[c].push_back(lay.perm[q]);
-    }
-    const int slice = *std::max_element(cnt.begin(), cnt.end()) * B;
-    const int cap = tile_capacity(slice);
-    const int lim = cap / 3;
-    std::vector<std::vector<int4>> ent(cs);
-    std::vector<std::vector<int>> info(cs);
-    for (int l = 0; l < nlev; ++l) {
-        int q = S.lev_ptr[l];
-        const int qe = S.lev_ptr[l + 1];
-        for (int c = 0; c < cs; ++c) {
-            int q1 = q;
-            while (q1 < qe && stored_owner[q1] == c) ++q1;
-            // rows [q, q1) of level l belong to c: sub-chunks of <= lim bytes
-            int a = q;
-            do {
-                int b = a;
-                while (b < q1 && tile_entry_bytes(b + 1 - a, S.h_rowptr[a], S.h_rowptr[b + 1], B) <= lim) ++b;
-                if (b == a && a < q1) ++b; // (tile_order checked single rows fit)
-                const bool last = b >= q1;
-                const int zo = a < q1 ? local[a] * B : 0;
-                ent[c].push_back(make_int4(a, b, S.h_rowptr[a < n ? a : n - 1], S.h_rowptr[b < n ? b : n]));
-                if (a == b) ent[c].back() = make_int4(a, a, S.h_rowptr[a], S.h_rowptr[a]);
-                info[c].push_back((zo << 1) | (last ? 1 : 0));
-                a = b;
-            } while (a < q1);
-            q = q1;
-        }
-        if (q != qe) throw Error(ED_UNSUPPORTED, "tile sweep: level rows not CTA-major");
-    }
-    // forward: levels ascending; backward: the same entries with the levels in
-    // reverse (within a level any order; the barrier follows the level's last)
-    std::vector<int4> all_ent, bwd_ent;
-    std::vector<int> all_info, bwd_info, ent_ptr(cs + 1, 0), rown;
-    for (int c = 0; c < cs; ++c) {
-        all_ent.insert(all_ent.end(), ent[c].begin(), ent[c].end());
-        all_info.insert(all_info.end(), info[c].begin(), info[c].end());
-        const int ne = static_cast<int>(ent[c].size());
-        for (int e = ne - 1; e >= 0; --e) {
-            bwd_ent.push_back(ent[c][e]);
-            const bool first_of_level = e == 0 || (info[c][e - 1] & 1);
-            bwd_info.push_back((info[c][e] & ~1) | (first_of_level ? 1 : 0));
-        }
-        ent_ptr[c + 1] = static_cast<int>(all_ent.size());
-        own_ptr[c + 1] = own_ptr[c] + static_cast<int>(own[c].size());
-        rown.insert(rown.end(), own[c].begin(), own[c].end());
-    }
-    std::vector<int4> hdr(n);
-    std::vector<int> colz(S.nnzb);
-    for (int q = 0; q < n; ++q) {
-        int dp = -1;
-        for (int k = S.h_rowptr[q]; k < S.h_rowptr[q + 1]; ++k) {
-            const int sc = lay.inv[S.h_col[k]];
-            colz[k] = (stored_owner[sc] << 24) | (local[sc] * B * 8);
-            if (sc == q) dp = k;
-        }
-        hdr[q] = make_int4(S.h_rowptr[q], S.h_rowptr[q + 1], lay.perm[q], dp);
-    }
-    S.tile_cs = cs;
-    S.tile_slice = slice;
-    S.tile_cap = cap;
-    S.tent.upload(all_ent, s);
-    S.tent_ptr.upload(ent_ptr, s);
-    S.tent_info.upload(all_info, s);
-    S.tent_bwd.upload(bwd_ent, s);
-    S.tent_info_bwd.upload(bwd_info, s);
-    S.thdr.upload(hdr, s);
-    S.tcolz.upload(colz, s);
-    S.town.upload(rown, s);
-    S.town_ptr.upload(own_ptr, s);
-}
 
 // Push-sweep structures of a ring-ordered operator (kernels_ring.cu).
 static void ring_build(BsrStruct& S, const BsrLayout& lay, cudaStream_t s)
@@ -616,13 +470,75 @@ std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLay
         S.blocked = false;
         S.cluster = 0;
     }
-    if (lay.tile_cs > 0 && Rb == Cb && pat.nbr == pat.nbc) {
-        tile_build(S, lay, s);
-        S.blocked = false;
-        S.cluster = 0;
-    }
+    if (Rb == Cb && (Rb == 1 || Rb == 3) && pat.nbr == pat.nbc && S.leveled && S.nbr > 0) group_build(S, s);
     ED_CUDA(cudaStreamSynchronize(s)); // host vectors die at return
     return st;
+}
+
+void group_build(BsrStruct& S, cudaStream_t s)
+{
+    // narrow consecutive levels are merged while the group has <= grp_rows
+    // scalar rows; a level wider than a quarter of that is a group of its own
+    static const int grp_rows = std::getenv("ED_GROUP_ROWS") ? std::atoi(std::getenv("ED_GROUP_ROWS")) : 1024;
+    const int B = S.Rb, n = S.nbr, nlev = S.nlev();
+    std::vector<int4> grp;
+    std::vector<int> grp_of(n, -1);
+    for (int l = 0; l < nlev;) {
+        const int a = S.lev_ptr[l];
+        int e = l + 1;
+        int m = (S.lev_ptr[e] - a) * B;
+        if (grp_rows > 0 && 4 * m <= grp_rows)
+            while (e < nlev && m + (S.lev_ptr[e + 1] - S.lev_ptr[e]) * B <= grp_rows &&
+                   4 * (S.lev_ptr[e + 1] - S.lev_ptr[e]) * B <= grp_rows) {
+                m += (S.lev_ptr[e + 1] - S.lev_ptr[e]) * B;
+                ++e;
+            }
+        const int b = S.lev_ptr[e];
+        const bool multi = e - l > 1;
+        for (int r = a; r < b; ++r) grp_of[r] = multi ? static_cast<int>(grp.size()) : -1;
+        grp.push_back(make_int4(a, b, multi ? m : 0, 0));
+        l = e;
+    }
+    S.ngrp = static_cast<int>(grp.size());
+    std::vector<long long> toff(grp.size(), 0);
+    std::vector<int2> chunks;
+    int64_t tot = 0;
+    int maxm = 0;
+    for (size_t g = 0; g < grp.size(); ++g) {
+        const int m = grp[g].z;
+        toff[g] = tot;
+        if (m == 0) continue;
+        tot += static_cast<int64_t>(m) * (m + 1) / 2;
+        maxm = std::max(maxm, m);
+        for (int j0 = 0; j0 < m; j0 += 32) chunks.push_back(make_int2(static_cast<int>(g), j0));
+    }
+    S.grp_tinv = tot;
+    S.grp_maxm = maxm;
+    S.ntchunk = static_cast<int>(chunks.size());
+    const bool identity = S.h_inv.empty();
+    std::vector<unsigned char> code(S.nnzb, 0);
+    std::vector<int> gptr(n + 1, 0), gblk;
+    for (int sr = 0; sr < n; ++sr) {
+        const int row = identity ? sr : S.h_perm[sr];
+        for (int k = S.h_rowptr[sr]; k < S.h_rowptr[sr + 1]; ++k) {
+            const int c = S.h_col[k];
+            const int sc = identity ? c : S.h_inv[c];
+            if (c == row) code[k] = 3;
+            else if (grp_of[sr] >= 0 && grp_of[sc] == grp_of[sr]) code[k] = sc < sr ? 1 : 2;
+            if (grp_of[sr] >= 0 && code[k] != 0) gblk.push_back(k);
+        }
+        gptr[sr + 1] = static_cast<int>(gblk.size());
+    }
+    S.grp.upload(grp, s);
+    S.grp_toff.upload(toff, s);
+    S.bcode.upload(code, s);
+    S.gptr.upload(gptr, s);
+    if (gblk.empty()) gblk.push_back(0);
+    S.gblk.upload(gblk, s);
+    if (chunks.empty()) chunks.push_back(make_int2(0, 0));
+    S.tchunk.upload(chunks, s);
+    S.gbar.alloc(1);
+    S.gsbuf.alloc(std::max(maxm, 1));
 }
 
 std::vector<double> bsr_pack_values(const BsrStruct& st, const BsrLayout& lay, const std::vector<double>& bvals)

@@ -19,7 +19,6 @@ struct BlockSys {
     int Bv = 3;
     int nv = 0, np = 0;
     BlockPattern pA, pB, pC, pD;
-    std::vector<double> row_xyz; // optional: coordinates of the velocity block rows (tiled sweep partition)
     BsrLayout lA, lB, lC, lD;
     Bsr A, B, C, D;
     // S_hat symbolic (pattern of D - C diag(A)^-1 B, leveled) + position maps
@@ -147,7 +146,6 @@ struct Ctx {
     DevArray<int> tets;
     DevArray<double> grad_n, volume, tau;
     std::vector<int> h_tets;
-    std::vector<double> h_xyz; // node coordinates (ed_mesh_coords; optional, sweep partitioning only)
     int nfree = 0;
     std::vector<int> fidx, fnode; // node -> free index; free index -> node
     DevArray<int> d_fidx, d_fnode;

@@ -211,20 +211,19 @@ struct BsrStruct {
     DevArray<int> rpsrc;    // [npk] stored block index of each packed block
     DevArray<int> rown;     // [nbr] original rows in (CTA, local) order
     DevArray<int> rown_ptr; // [cs+1]
-    // tiled cluster sweep (kernels_tile.cu): rows owned by spatial tiles of a
-    // 16-CTA cluster, z of each tile in its CTA's shared memory
-    int tile_cs = 0;
-    int tile_slice = 0;      // max scalars of z owned by one CTA
-    int tile_cap = 0;        // ring bytes per CTA
-    DevArray<int4> tent;     // per-CTA sub-chunk entries {s0, s1, kb, ke}
-    DevArray<int> tent_ptr;  // [cs+1]
-    DevArray<int> tent_info; // local z index of the first row << 1 | last entry of its level
-    DevArray<int4> tent_bwd; // backward sweep: levels in reverse
-    DevArray<int> tent_info_bwd;
-    DevArray<int4> thdr;     // [nbr] {kb, ke, original row, diagonal block}
-    DevArray<int> tcolz;     // [nnzb] owner << 24 | byte offset of the column's z in the owner's slice
-    DevArray<int> town;      // [nbr] original rows in (CTA, local) order
-    DevArray<int> town_ptr;  // [cs+1]
+    // level-group sweep (kernels_group.cu): consecutive narrow levels merged
+    // into groups whose in-group lower triangle is inverted per value change
+    int ngrp = 0;                 // 0: no group schedule
+    int grp_maxm = 0;             // scalar rows of the largest multi-level group
+    int64_t grp_tinv = 0;         // packed T^-1 doubles per direction (0: all groups single-level)
+    int ntchunk = 0;              // (group, 32-column) chunks of the T^-1 build
+    DevArray<int4> grp;           // [ngrp] {r0, r1, m (0: single level), 0} stored rows
+    DevArray<long long> grp_toff; // [ngrp] offset of the group's packed T^-1
+    DevArray<unsigned char> bcode; // [nnzb] 0 other group, 1 in-group lower, 2 in-group upper, 3 diagonal
+    DevArray<int> gptr, gblk;     // in-group blocks per stored row (multi-level groups)
+    DevArray<int2> tchunk;        // [ntchunk] {group, j0}
+    DevArray<unsigned int> gbar;  // grid-barrier counter
+    DevArray<double> gsbuf;       // [grp_maxm] phase-A sums of the current group
     // host mirrors
     std::vector<int> h_rowptr, h_col, h_perm, h_inv;
     int nlev() const { return static_cast<int>(lev_ptr.size()) - 1; }
@@ -249,8 +248,6 @@ struct Bsr {
 struct BsrLayout {
     std::vector<int> perm, inv, lev_ptr;
     int ring_cs = 0; // > 0: rows of each level are dealt round-robin to ring_cs CTAs, CTA-major (ring_order)
-    int tile_cs = 0; // > 0: rows are owned by tile_cs spatial tiles, CTA-major inside each level (tile_order)
-    std::vector<int> tile_owner; // [nbr] tile of each original row
     std::vector<int64_t> addr; // stored block index per pattern block
 };
 
@@ -272,14 +269,6 @@ void gs_level_order(const BlockPattern& pat, std::vector<int>& order, std::vecto
 // (round-robin deal) and return the cluster size; else 0 (order unchanged).
 int ring_order(const BlockPattern& pat, int B, std::vector<int>& order, const std::vector<int>& level_of_pos,
                int nlev);
-// Tiled cluster sweep eligibility (kernels_tile.cu): with row coordinates
-// (3 per block row) and a vector that fits a 16-CTA cluster's shared memory,
-// partition the rows into spatial tiles (equal-count x/y bisection), reorder
-// each level CTA-major and return the cluster size (owner per row in `owner`).
-int tile_order(const BlockPattern& pat, int B, const std::vector<double>& xyz, std::vector<int>& order,
-               const std::vector<int>& level_of_pos, int nlev, std::vector<int>& owner);
-int tile_capacity(int slice);
-void sgs_tile(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s);
 bool pattern_symmetric(const BlockPattern& pat);
 // lanes per block row of the BSR kernels for an average row length (bsr_host.cpp)
 int auto_lanes(double avg_blocks, int entries);
@@ -306,6 +295,18 @@ void blocked_dense(const Bsr& A, DevArray<double>& dense, cudaStream_t s);
 // blocked half sweep (kernels_blocked.cu), A.st->blocked
 void sgs_blocked(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s,
                  const double* dense);
+// 0: level-group sweeps (default), 1: ED_SWEEP=legacy
+int sweep_mode();
+// per-value-change auxiliary data of a Gauss-Seidel operator: the group
+// sweep's T^-1 (or the legacy sweeps' packed / group blocks)
+void sweep_prepare(const Bsr& A, const double* invd, DevArray<double>& aux, cudaStream_t s);
+// level-group half sweep (kernels_group.cu), A.st->ngrp > 0; X = group_prepare output
+void sgs_group(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s,
+               const double* X);
+// packed in-group triangular inverses of both sweep directions (values and inv_diag as of the call)
+void group_prepare(const Bsr& A, const double* invd, DevArray<double>& X, cudaStream_t s);
+// group schedule of a leveled square operator (bsr_host.cpp)
+void group_build(BsrStruct& S, cudaStream_t s);
 // cluster push half sweep (kernels_ring.cu), A.st->ring_cs > 0; packed = ring_pack output
 void sgs_ring(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s,
               const double* packed);

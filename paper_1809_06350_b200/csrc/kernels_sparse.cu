@@ -16,6 +16,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "ed_internal.hpp"
@@ -639,8 +640,8 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
     if (S.nitems == 0) return;
     const int nlev = S.nlev();
     const BsrArgs a = args_of(A);
-    if (S.tile_cs > 0) {
-        sgs_tile(A, b, z, invd, fwd, s);
+    if (S.ngrp > 0 && sweep_mode() == 0) {
+        sgs_group(A, b, z, invd, fwd, s, dense);
         return;
     }
     if (S.ring_cs > 0) {
@@ -758,12 +759,25 @@ void sgs_sweep(const Bsr& A, const double* b, double* z, const double* invd, boo
     // pointers, b and inv_diag read, z read and written
     const double bytes = static_cast<double>(S.nnzb) * (8.0 * B * B + 4.0) + 4.0 * (S.nbr + 1) +
                          4.0 * 8.0 * S.nbr * B;
- const char* kname = S.tile_cs > 0 ? "k_sgs_tile" : S.ring_cs > 0 ? "k_sgs_push" : S.blocked ? "k_sgs_blocked" : S.cluster > 0 ? "k_sgs_cluster" : S.chain ? "k_sgs_chain"
+ const char* kname = S.ngrp > 0 && sweep_mode() == 0 ? "k_group_sweep" : S.ring_cs > 0 ? "k_sgs_push" : S.blocked ? "k_sgs_blocked" : S.cluster > 0 ? "k_sgs_cluster" : S.chain ? "k_sgs_chain"
                                                                                               : "k_sgs_flow";
     AcctScope acct(s, kname, bytes);
     if (B == 1) return launch_sgs<1>(A, b, z, invd, forward, s, dense);
     if (B == 3) return launch_sgs<3>(A, b, z, invd, forward, s, dense);
     throw Error(ED_UNSUPPORTED, "sgs: unsupported block size");
+}
+
+int sweep_mode()
+{
+    // ED_SWEEP=legacy: the round-1 sweeps (dataflow / cluster push / blocked)
+    static const int mode = std::getenv("ED_SWEEP") && std::string(std::getenv("ED_SWEEP")) == "legacy" ? 1 : 0;
+    return mode;
+}
+
+void sweep_prepare(const Bsr& A, const double* invd, DevArray<double>& aux, cudaStream_t s)
+{
+    if (A.st->ngrp > 0 && sweep_mode() == 0) return group_prepare(A, invd, aux, s);
+    blocked_dense(A, aux, s);
 }
 
 void jacobi_update(double* z, const double* b, const double* t, const double* invd, double w, int64_t n,

@@ -359,7 +359,7 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
                 d.A = &d.Aown;
             }
             d.invd = std::move(D.invd);
-            blocked_dense(*d.A, d.gdense, s);
+            sweep_prepare(*d.A, d.invd.p, d.gdense, s);
             d.s.alloc(d.n);
             if (l > 0) {
                 d.r.alloc(d.n);
@@ -406,7 +406,7 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
             d.A = &d.Aown;
         }
         d.invd.upload(H.inv_diag, s);
-        blocked_dense(*d.A, d.gdense, s);
+        sweep_prepare(*d.A, d.invd.p, d.gdense, s);
         d.s.alloc(d.n);
         if (l > 0) {
             d.r.alloc(d.n);

@@ -18,13 +18,9 @@ void BlockSys::build_structure(cudaStream_t s)
     std::vector<int> order, lvl;
     int nlev = 0;
     gs_level_order(pA, order, lvl, nlev);
-    std::vector<int> towner;
-    const int tcs = tile_order(pA, Bv, row_xyz, order, lvl, nlev, towner);
-    const int rcs = tcs > 0 ? 0 : ring_order(pA, Bv, order, lvl, nlev);
+    const int rcs = ring_order(pA, Bv, order, lvl, nlev);
     lA = make_layout(pA, order, lvl);
     lA.ring_cs = rcs;
-    lA.tile_cs = tcs;
-    lA.tile_owner = std::move(towner);
     lB = make_layout(pB, order, lvl); // same slicing as A
     std::vector<int> porder(pD.nbr);
     std::iota(porder.begin(), porder.end(), 0);
@@ -250,12 +246,6 @@ void ctx_build_mesh_system(Ctx& c)
     S.pD = PN;
     srcD.resize(PN.nnzb());
     std::iota(srcD.begin(), srcD.end(), 0);
-    S.row_xyz.clear();
-    if (static_cast<int64_t>(c.h_xyz.size()) == 3LL * N) {
-        S.row_xyz.resize(3LL * F);
-        for (int f = 0; f < F; ++f)
-            for (int d = 0; d < 3; ++d) S.row_xyz[3LL * f + d] = c.h_xyz[3LL * fnode[f] + d];
-    }
     S.build_structure(s);
     auto stored_src = [&](const BsrLayout& L, const std::vector<int64_t>& src, DevArray<int>& out) {
         std::vector<int> v(src.size(), -1);

@@ -7,7 +7,8 @@ swapping t[2] and t[3] (:94-103), ``volume = det/6``, shape-function gradients
 from the rows of the inverse edge matrix (:106-115), ``h`` = longest edge
 (:117-121) and boundary facets per local face (:125-154).  Every expression
 keeps the reference's operation order, so the arrays are bitwise identical
-to the reference's (checked by tests/test_mesh_cpu.py against oracle/_ref).
+to the reference's (checked by tests/test_oracle_cpu.py::test_mesh_tau_loads_bitwise_equal_to_reference
+against oracle/_ref).
 """
 from __future__ import annotations
 

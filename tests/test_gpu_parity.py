@@ -515,3 +515,17 @@ def test_solve_block_system_variants(cfg0, oracle, parity_log, kind):
     _assert_stats(sg, sr)
     _assert_history(hg, hr)
     assert _rel(xg, xr) < X_TOL
+
+
+def test_reference_side_cpp_binding_runs():
+    """The reference-side C++ binding of INTEGRATION.md (built by oracle/Makefile
+    against the reference headers): one corrector pass built with the
+    reference API, assembled and solved through include/elastodyn_b200.hpp,
+    against the reference's own assemble/solve on the same state."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "first_pass_shim")
+    assert os.path.exists(exe), "build() compiles the binding (oracle/Makefile)"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, (r.stdout, r.stderr)
