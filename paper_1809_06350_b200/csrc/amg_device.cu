@@ -910,6 +910,7 @@ Bsr bsr_leveled(const DBsrRaw& m, cudaStream_t s)
     ED_CUDA(cudaMemcpyAsync(rp.data(), m.rowptr, rp.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
     if (m.nnzb) ED_CUDA(cudaMemcpyAsync(pat.col.data(), m.col, m.nnzb * sizeof(int), cudaMemcpyDeviceToHost, s));
     ED_CUDA(cudaStreamSynchronize(s));
+    HostSection hsec;
     pat.rowptr.assign(rp.begin(), rp.end());
     lap("download");
     if (!pattern_symmetric(pat)) throw Error(ED_UNSUPPORTED, "Gauss-Seidel operator pattern is not symmetric");
@@ -1008,24 +1009,26 @@ DevSetupResult amg_build_device_impl(const Bsr& A0, const AmgOpts& opts, cudaStr
         T.lap(s, "strength", lvl, n, amb);
         // neighbour lists -> host aggregation
         std::vector<int64_t> nptr(n + 1, 0);
+        std::vector<int> agg_of_node;
+        int n_agg = 0;
         {
             const std::vector<int> c = scnt.to_host(s);
             for (int I = 0; I < n; ++I) nptr[I + 1] = nptr[I] + c[I];
         }
-        std::vector<int> nbr(nptr[n]);
         {
+            std::vector<int> nbr(nptr[n]);
             const std::vector<unsigned char> hs = sym.to_host(s);
             const std::vector<int> hrp = A.rowptr.to_host(s), hcol = A.col.to_host(s);
+            HostSection hsec;
             for (int I = 0; I < n; ++I) {
                 int64_t o = nptr[I];
                 for (int kk = hrp[I]; kk < hrp[I + 1]; ++kk)
                     if (hs[kk]) nbr[o++] = hcol[kk];
             }
+            n_agg = amg_aggregate(nptr, nbr, agg_of_node);
         }
         flag.release();
         sym.release();
-        std::vector<int> agg_of_node;
-        const int n_agg = amg_aggregate(nptr, nbr, agg_of_node);
         T.lap(s, "aggregate", lvl, n_agg, 0);
         if (n_agg <= 0 || n_agg >= n) {
             if (res.levels.empty()) {
@@ -1041,10 +1044,14 @@ DevSetupResult amg_build_device_impl(const Bsr& A0, const AmgOpts& opts, cudaStr
         }
         // tentative prolongator (host, tiny)
         const int nrows = n * Bs;
-        std::vector<int> agg_of_row(nrows);
-        for (int r = 0; r < nrows; ++r) agg_of_row[r] = agg_of_node[r / Bs];
         std::vector<double> Bc;
-        const HostCsr Pt_h = amg_tentative(nrows, k, agg_of_row, n_agg, Bn, Bc);
+        HostCsr Pt_h;
+        {
+            HostSection hsec;
+            std::vector<int> agg_of_row(nrows);
+            for (int r = 0; r < nrows; ++r) agg_of_row[r] = agg_of_node[r / Bs];
+            Pt_h = amg_tentative(nrows, k, agg_of_row, n_agg, Bn, Bc);
+        }
         DBsr Pt = upload_block(Pt_h, Bs, k, s);
         T.lap(s, "tentative", lvl, Pt.nbr, Pt.nnzb);
         // inverse diagonal + spectral radius of D^-1 A (amg.cpp:170-185)
@@ -1075,6 +1082,7 @@ DevSetupResult amg_build_device_impl(const Bsr& A0, const AmgOpts& opts, cudaStr
                 after_launch("k_spmv_seq");
                 ED_CUDA(cudaMemcpyAsync(hbuf, w.p, sizeof(double) * nrows, cudaMemcpyDeviceToHost, s));
                 ED_CUDA(cudaStreamSynchronize(s));
+                HostSection hsec;
                 if (it == 9) hw_prev.swap(hw); // w of iteration 8 (v of iteration 9 = hw_prev * inv_prev)
                 hw.assign(hbuf, hbuf + nrows);
                 const double nrm = amg_seq_norm(hw);
@@ -1131,6 +1139,7 @@ DevSetupResult amg_build_device_impl(const Bsr& A0, const AmgOpts& opts, cudaStr
     L.inv_diag = L.invd.to_host(s);
     check_coarse_size(nr, static_cast<int>(res.levels.size()));
     const HostCsr Ah = to_host_csr(A, s);
+    HostSection hsec;
     std::vector<double> dense(static_cast<size_t>(nr) * nr, 0.0);
     for (int r = 0; r < nr; ++r)
         for (int64_t kk = Ah.rowptr[r]; kk < Ah.rowptr[r + 1]; ++kk)

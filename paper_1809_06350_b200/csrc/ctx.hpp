@@ -114,6 +114,7 @@ struct DevHierarchy {
 struct WorkSys {
     int Bv = 3, nv = 0, np = 0;
     Bsr A, B, C, D, S;
+    CoupledOp K; // the same system as one 4x4 BSR (mesh-assembled systems; n_nodes 0 otherwise)
     DevArray<double> w; // scaling weights (nv + np)
     bool scaled = false;
 };

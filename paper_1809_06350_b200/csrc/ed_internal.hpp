@@ -44,6 +44,13 @@ std::string& prof_tag(); // ED_PROFILE attribution tag (e.g. hierarchy/level)
 // Host milliseconds spent in cudaMalloc/cudaFree (diagnostics, ED_AMG_VERBOSE).
 double& alloc_ms();
 double now_ms_host();
+// Host milliseconds of pure host work on this thread (AMG aggregation, tentative
+// prolongator, level schedules, COD): HostSection scopes add to it.
+double& host_ms_acc();
+struct HostSection {
+    double t0 = now_ms_host();
+    ~HostSection() { host_ms_acc() += now_ms_host() - t0; }
+};
 
 // Stream that device arrays allocated on this thread are ordered on (the
 // calling context's stream inside every C-ABI entry point; null outside:
@@ -217,6 +224,8 @@ struct BsrStruct {
     int grp_maxm = 0;             // scalar rows of the largest multi-level group
     int64_t grp_tinv = 0;         // packed T^-1 doubles per direction (0: all groups single-level)
     int ntchunk = 0;              // (group, 32-column) chunks of the T^-1 build
+    bool grp_cluster = false;     // sweep inside one 16-CTA cluster (cheap barriers) instead of the whole grid
+    bool grp_use = false;         // the group sweep is this operator's sweep (narrow, deep schedules)
     DevArray<int4> grp;           // [ngrp] {r0, r1, m (0: single level), 0} stored rows
     DevArray<long long> grp_toff; // [ngrp] offset of the group's packed T^-1
     DevArray<unsigned char> bcode; // [nnzb] 0 other group, 1 in-group lower, 2 in-group upper, 3 diagonal
@@ -243,6 +252,25 @@ struct Bsr {
         val.copy_from(o.val, s);
     }
 };
+
+// Scaled coupled operator K = [A B; C D] as a 4x4 BSR over the node graph
+// (kernels_coupled.cu): natural node order, the D plane's pattern, 16 doubles
+// per block; velocity rows/columns of fixed nodes zero.
+struct CoupledOp {
+    int n_nodes = 0;
+    int64_t nnzb = 0;
+    const int* rowptr = nullptr; // [n_nodes + 1] (the D plane's)
+    const int* col = nullptr;    // [nnzb]
+    const int* fidx = nullptr;   // node -> free velocity index (-1: fixed)
+    DevArray<double> val;        // [nnzb][16]
+    // algorithmic bytes of one y = K x: blocks + one index, row pointers, x and y
+    double bytes(int64_t n_unknowns) const
+    {
+        return static_cast<double>(nnzb) * 132.0 + 4.0 * (n_nodes + 1) + 16.0 * static_cast<double>(n_unknowns);
+    }
+};
+void k44_build(const CoupledOp& K, const double* k4, const double* w, int nv, cudaStream_t s);
+void spmv44(const CoupledOp& K, const double* x, double* y, int nv, int np, cudaStream_t s);
 
 // Where each block of a pattern (block-CSR order) lands in the stored order.
 struct BsrLayout {
@@ -295,8 +323,9 @@ void blocked_dense(const Bsr& A, DevArray<double>& dense, cudaStream_t s);
 // blocked half sweep (kernels_blocked.cu), A.st->blocked
 void sgs_blocked(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s,
                  const double* dense);
-// 0: level-group sweeps (default), 1: ED_SWEEP=legacy
+// ED_SWEEP: 0 default (group sweep where BsrStruct::grp_use), 1 legacy, 2 group everywhere
 int sweep_mode();
+bool group_sweep_on(const BsrStruct& S);
 // per-value-change auxiliary data of a Gauss-Seidel operator: the group
 // sweep's T^-1 (or the legacy sweeps' packed / group blocks)
 void sweep_prepare(const Bsr& A, const double* invd, DevArray<double>& aux, cudaStream_t s);

@@ -35,6 +35,8 @@ namespace edb {
 namespace {
 
 constexpr int kGT = 256; // threads per CTA of the sweep kernel
+constexpr int kGroupMaxRows = 1024;
+constexpr int kGroupCluster = 16; // CTAs of the cluster-scoped sweep (non-portable size) // scalar rows of a multi-level group (T^-1 row prefetch depth)
 
 struct GrpArgs {
     const int* rowptr;
@@ -63,14 +65,35 @@ __device__ __forceinline__ void g_red_release(unsigned int* p, unsigned int v)
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// all CTAs of the (co-resident) grid; `target` counts arrivals so far
-__device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& target)
+// Grid barrier over all (co-resident) CTAs, split in two so that loads of the
+// next step's z-independent data can be issued between arrive and wait (a
+// release would otherwise wait for them).  `target` counts arrivals so far.
+template <bool CL>
+__device__ __forceinline__ void bar_arrive(unsigned int* ctr)
 {
+    if (CL) {
+        // cluster scope: the hardware barrier (release orders this thread's z / s stores)
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        return;
+    }
     __syncthreads();
+    if (threadIdx.x == 0) g_red_release(ctr, 1u);
+}
+
+template <bool CL>
+__device__ __forceinline__ void bar_wait(unsigned int* ctr, unsigned int& target)
+{
+    if (CL) {
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        return;
+    }
     target += gridDim.x;
     if (threadIdx.x == 0) {
-        g_red_release(ctr, 1u);
+        // bounded spin: a grid whose CTAs are not all resident would wait
+        // forever; trap after ~10 s instead of hanging the device
+        const long long t0 = clock64();
         while (g_ld_acquire(ctr) < target) {
+            if (clock64() - t0 > 20000000000LL) __trap();
         }
     }
     __syncthreads();
@@ -91,140 +114,209 @@ __device__ __forceinline__ int local_of(int sr, int c, int r0, int r1)
     return FWD ? (sr - r0) * B + c : (r1 - 1 - sr) * B + (B - 1 - c);
 }
 
-// Single-level group: the whole Gauss-Seidel update of stored row sr (lanes
-// of a group of L split its blocks; current z everywhere; the leader solves
-// the diagonal block in sweep order).
-template <int B, int L, bool FWD>
-__device__ __forceinline__ void row_update(const GrpArgs& a, const double* __restrict__ bvec,
-                                           const double* __restrict__ invd, double* z, int sr, int lane)
+// Everything of one row a lane needs that does not depend on z: its first PF
+// blocks (column, in-group code, values) and, for the group leader, b, inv_diag
+// and the diagonal block.  Loaded for the NEXT group before the grid barrier,
+// so after the barrier only the z gathers sit on the critical path.
+template <int B, int PF>
+struct GRow {
+    int row, kb, ke;
+    bool valid;
+    int c[PF];
+    int code[PF];
+    double v[PF][B * B];
+    double b[B], id[B], D[B * B], zs[B];
+};
+
+template <int B, int L, int PF>
+__device__ __forceinline__ void grow_load(const GrpArgs& a, const double* __restrict__ bvec,
+                                          const double* __restrict__ invd, const double* z, int sr, bool valid,
+                                          int lane, GRow<B, PF>& P)
 {
-    const int row = a.perm ? a.perm[sr] : sr;
-    const int kb = a.rowptr[sr], ke = a.rowptr[sr + 1];
+    P.valid = valid;
+    P.row = valid ? (a.perm ? a.perm[sr] : sr) : 0;
+    P.kb = valid ? a.rowptr[sr] + lane : 0;
+    P.ke = valid ? a.rowptr[sr + 1] : 0;
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+        const int k = P.kb + q * L;
+        const bool in = k < P.ke;
+        P.c[q] = in ? __ldg(a.col + k) : -1;
+        P.code[q] = in ? a.bcode[k] : -1;
+#pragma unroll
+        for (int e = 0; e < B * B; ++e) P.v[q][e] = in ? __ldg(a.val + static_cast<int64_t>(k) * (B * B) + e) : 0.0;
+    }
+    if (valid && lane == 0) {
+        const int dp = a.dpos[sr];
+#pragma unroll
+        for (int d = 0; d < B; ++d) {
+            const int64_t i = static_cast<int64_t>(P.row) * B + d;
+            P.b[d] = __ldg(bvec + i);
+            P.id[d] = __ldg(invd + i);
+            P.zs[d] = __ldcg(z + i); // only this row writes z[row] during the sweep
+        }
+#pragma unroll
+        for (int e = 0; e < B * B; ++e) P.D[e] = dp >= 0 ? __ldg(a.val + static_cast<int64_t>(dp) * (B * B) + e) : 0.0;
+    }
+}
+
+// does the block's scalar (r, d) enter the sum (everything not in T_G)?
+template <bool FWD, bool MULTI>
+__device__ __forceinline__ bool takes(int code, int r, int d)
+{
+    if (!MULTI) return code != 3;                         // single level: all off-diagonal blocks
+    if (code == 3) return FWD ? d > r : d < r;             // diagonal block: the far side of the sweep
+    return code == 0 || code == (FWD ? 2 : 1);             // other groups; in-group blocks not yet swept
+}
+
+// Row sums over the z-dependent part.  MULTI = false: the full Gauss-Seidel
+// update of the row (single-level group; the leader solves the diagonal block
+// in sweep order and writes z).  MULTI = true: s_i = b_i - (A - T_G)_i z into
+// the group's local buffer (phase A).
+template <int B, int L, int PF, bool FWD, bool MULTI>
+__device__ __forceinline__ void grow_finish(const GrpArgs& a, double* z, double* sbuf, int sr, int r0, int r1,
+                                            int lane, const GRow<B, PF>& P)
+{
     double acc[B];
 #pragma unroll
     for (int r = 0; r < B; ++r) acc[r] = 0.0;
-    for (int k = kb + lane; k < ke; k += L) {
-        const int c = __ldg(a.col + k);
-        if (c == row) continue;
-        const double* vp = a.val + static_cast<int64_t>(k) * (B * B);
-        double zv[B];
+    double zv[PF][B];
 #pragma unroll
-        for (int d = 0; d < B; ++d) zv[d] = __ldcg(z + static_cast<int64_t>(c) * B + d);
+    for (int q = 0; q < PF; ++q) {
+        const int64_t cc = P.c[q] >= 0 ? P.c[q] : 0;
+#pragma unroll
+        for (int d = 0; d < B; ++d) zv[q][d] = __ldcg(z + cc * B + d);
+    }
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+        if (P.c[q] < 0) continue;
 #pragma unroll
         for (int d = 0; d < B; ++d)
 #pragma unroll
-            for (int r = 0; r < B; ++r) acc[r] = fma(__ldg(vp + r * B + d), zv[d], acc[r]);
+            for (int r = 0; r < B; ++r)
+                if (takes<FWD, MULTI>(P.code[q], r, d)) acc[r] = fma(P.v[q][r * B + d], zv[q][d], acc[r]);
     }
-#pragma unroll
-    for (int r = 0; r < B; ++r) acc[r] = lane_sum<L>(acc[r]);
-    if (lane == 0) {
-        const int dp = a.dpos[sr];
-        double zs[B], D[B * B];
-#pragma unroll
-        for (int d = 0; d < B; ++d) zs[d] = __ldcg(z + static_cast<int64_t>(row) * B + d);
-#pragma unroll
-        for (int e = 0; e < B * B; ++e) D[e] = dp >= 0 ? __ldg(a.val + static_cast<int64_t>(dp) * (B * B) + e) : 0.0;
-#pragma unroll
-        for (int ci = 0; ci < B; ++ci) {
-            const int c = FWD ? ci : B - 1 - ci;
-            const int64_t i = static_cast<int64_t>(row) * B + c;
-            double v = __ldg(bvec + i) - acc[c];
-#pragma unroll
-            for (int d = 0; d < B; ++d)
-                if (d != c) v -= D[c * B + d] * zs[d];
-            zs[c] = v * __ldg(invd + i);
-        }
-#pragma unroll
-        for (int d = 0; d < B; ++d) z[static_cast<int64_t>(row) * B + d] = zs[d];
-    }
-}
-
-// Multi-level group, phase A: s_i = b_i - sum of the row's entries that are
-// not in T_G (every block of another group; in-group blocks on the far side
-// of the sweep; the diagonal block's entries after i in sweep order), all
-// with the current z.
-template <int B, int L, bool FWD>
-__device__ __forceinline__ void row_rhs(const GrpArgs& a, const double* __restrict__ bvec, const double* z,
-                                        double* sbuf, int sr, int r0, int r1, int lane)
-{
-    const int row = a.perm ? a.perm[sr] : sr;
-    const int kb = a.rowptr[sr], ke = a.rowptr[sr + 1];
-    double acc[B];
-#pragma unroll
-    for (int r = 0; r < B; ++r) acc[r] = 0.0;
-    for (int k = kb + lane; k < ke; k += L) {
-        const int code = a.bcode[k];
+    for (int k = P.kb + PF * L; k < P.ke; k += L) {
         const int c = __ldg(a.col + k);
+        const int code = a.bcode[k];
         const double* vp = a.val + static_cast<int64_t>(k) * (B * B);
-        double zv[B];
 #pragma unroll
-        for (int d = 0; d < B; ++d) zv[d] = __ldcg(z + static_cast<int64_t>(c) * B + d);
-        if (code == 3) {
+        for (int d = 0; d < B; ++d) {
+            const double zz = __ldcg(z + static_cast<int64_t>(c) * B + d);
 #pragma unroll
             for (int r = 0; r < B; ++r)
-#pragma unroll
-                for (int d = 0; d < B; ++d)
-                    if (FWD ? d > r : d < r) acc[r] = fma(__ldg(vp + r * B + d), zv[d], acc[r]);
-        } else if (code == 0 || code == (FWD ? 2 : 1)) {
-#pragma unroll
-            for (int d = 0; d < B; ++d)
-#pragma unroll
-                for (int r = 0; r < B; ++r) acc[r] = fma(__ldg(vp + r * B + d), zv[d], acc[r]);
+                if (takes<FWD, MULTI>(code, r, d)) acc[r] = fma(__ldg(vp + r * B + d), zz, acc[r]);
         }
     }
 #pragma unroll
     for (int r = 0; r < B; ++r) acc[r] = lane_sum<L>(acc[r]);
-    if (lane == 0) {
+    if (!P.valid || lane != 0) return;
+    if (MULTI) {
 #pragma unroll
-        for (int c = 0; c < B; ++c)
-            sbuf[local_of<B, FWD>(sr, c, r0, r1)] = __ldg(bvec + static_cast<int64_t>(row) * B + c) - acc[c];
+        for (int c = 0; c < B; ++c) sbuf[local_of<B, FWD>(sr, c, r0, r1)] = P.b[c] - acc[c];
+        return;
     }
+    double zs[B];
+#pragma unroll
+    for (int d = 0; d < B; ++d) zs[d] = P.zs[d];
+#pragma unroll
+    for (int ci = 0; ci < B; ++ci) {
+        const int c = FWD ? ci : B - 1 - ci;
+        double v = P.b[c] - acc[c];
+#pragma unroll
+        for (int d = 0; d < B; ++d)
+            if (d != c) v -= P.D[c * B + d] * zs[d];
+        zs[c] = v * P.id[c];
+    }
+#pragma unroll
+    for (int d = 0; d < B; ++d) z[static_cast<int64_t>(P.row) * B + d] = zs[d];
 }
 
-// One half sweep: persistent grid, groups in sweep order.
-template <int B, int L, bool FWD>
-__global__ void __launch_bounds__(kGT) k_group_sweep(GrpArgs a, const double* __restrict__ bvec, double* z,
+// One half sweep: persistent grid, groups in sweep order.  Rows of a group are
+// dealt round-robin over the CTAs first (lane group lg of CTA b takes row
+// b + lg * grid), so a level's rows spread over the whole GPU; trip counts
+// are CTA-uniform, so every lane reaches the shuffles.
+template <int B, int L, bool FWD, bool CL>
+__global__ void __launch_bounds__(kGT, 1) k_group_sweep(GrpArgs a, const double* __restrict__ bvec, double* z,
                                                      const double* __restrict__ invd, const double* __restrict__ X,
                                                      double* sbuf, unsigned int* bar)
 {
-    constexpr int GPC = kGT / L; // lane groups per CTA
+    constexpr int PF = B == 3 ? 3 : 4;  // blocks per lane prefetched ahead of the barrier
+    constexpr int XQ = kGroupMaxRows / 32; // T^-1 row entries per lane prefetched ahead of phase B
+    constexpr int GPC = kGT / L;         // lane groups per CTA
     const int lg = threadIdx.x / L, lane = threadIdx.x % L;
     const int warp = threadIdx.x / 32, wl = threadIdx.x % 32;
+    const int stride = GPC * gridDim.x;
     unsigned int target = 0;
+    GRow<B, PF> P;
+    auto sr_of = [&](int r0, int r1, int q) { return FWD ? r0 + q : r1 - 1 - q; };
+    {
+        const int4 gi = a.grp[FWD ? 0 : a.ngrp - 1];
+        const int q = blockIdx.x + lg * gridDim.x;
+        grow_load<B, L, PF>(a, bvec, invd, z, sr_of(gi.x, gi.y, q), q < gi.y - gi.x, lane, P);
+    }
     for (int t = 0; t < a.ngrp; ++t) {
         const int g = FWD ? t : a.ngrp - 1 - t;
         const int4 gi = a.grp[g];
         const int r0 = gi.x, r1 = gi.y, m = gi.z;
         const int nr = r1 - r0;
-        // rows dealt round-robin over CTAs first (a level's rows spread over the whole GPU)
         if (m == 0) {
-            for (int q = blockIdx.x + lg * gridDim.x; q < nr; q += GPC * gridDim.x) {
-                const int sr = FWD ? r0 + q : r1 - 1 - q;
-                row_update<B, L, FWD>(a, bvec, invd, z, sr, lane);
+            for (int q0 = 0; q0 < nr; q0 += stride) {
+                const int q = q0 + blockIdx.x + lg * gridDim.x;
+                if (q0 > 0) grow_load<B, L, PF>(a, bvec, invd, z, sr_of(r0, r1, q), q < nr, lane, P);
+                grow_finish<B, L, PF, FWD, false>(a, z, sbuf, sr_of(r0, r1, q), r0, r1, lane, P);
             }
-            grid_barrier(bar, target);
-            continue;
-        }
-        for (int q = blockIdx.x + lg * gridDim.x; q < nr; q += GPC * gridDim.x)
-            row_rhs<B, L, FWD>(a, bvec, z, sbuf, r0 + q, r0, r1, lane);
-        grid_barrier(bar, target);
-        // phase B: z_G = T^-1 s_G, one warp per scalar row of the group
-        const double* Xg = X + a.toff[g];
-        for (int i = blockIdx.x + warp * gridDim.x; i < m; i += (kGT / 32) * gridDim.x) {
-            const double* xr = Xg + static_cast<int64_t>(i) * (i + 1) / 2;
-            double acc = 0.0;
+        } else {
+            for (int q0 = 0; q0 < nr; q0 += stride) {
+                const int q = q0 + blockIdx.x + lg * gridDim.x;
+                if (q0 > 0) grow_load<B, L, PF>(a, bvec, invd, z, sr_of(r0, r1, q), q < nr, lane, P);
+                grow_finish<B, L, PF, FWD, true>(a, z, sbuf, sr_of(r0, r1, q), r0, r1, lane, P);
+            }
+            bar_arrive<CL>(bar);
+            // this warp's first phase-B row of T^-1 into registers during the barrier
+            const double* Xg = X + a.toff[g];
+            const int i0 = blockIdx.x + warp * gridDim.x;
+            double xv[XQ];
+            const double* xr0 = Xg + static_cast<int64_t>(i0) * (i0 + 1) / 2;
+#pragma unroll
+            for (int q = 0; q < XQ; ++q) {
+                const int j = wl + 32 * q;
+                xv[q] = (i0 < m && j <= i0) ? __ldg(xr0 + j) : 0.0;
+            }
+            bar_wait<CL>(bar, target);
+            // phase B: z_G = T^-1 s_G, one warp per scalar row of the group
+            for (int i = i0; i < m; i += (kGT / 32) * gridDim.x) {
+                const double* xr = Xg + static_cast<int64_t>(i) * (i + 1) / 2;
+                double acc = 0.0;
+                if (i == i0) {
+#pragma unroll
+                    for (int q = 0; q < XQ; ++q) {
+                        const int j = wl + 32 * q;
+                        if (j <= i) acc = fma(xv[q], __ldcg(sbuf + j), acc);
+                    }
+                    for (int j = wl + 32 * XQ; j <= i; j += 32) acc = fma(__ldg(xr + j), __ldcg(sbuf + j), acc);
+                } else {
 #pragma unroll 4
-            for (int j = wl; j <= i; j += 32) acc = fma(__ldg(xr + j), __ldcg(sbuf + j), acc);
-            acc = lane_sum<32>(acc);
-            if (wl == 0) {
-                const int p = i / B, c = i % B;
-                const int sr = FWD ? r0 + p : r1 - 1 - p;
-                const int cc = FWD ? c : B - 1 - c;
-                const int row = a.perm ? a.perm[sr] : sr;
-                z[static_cast<int64_t>(row) * B + cc] = acc;
+                    for (int j = wl; j <= i; j += 32) acc = fma(__ldg(xr + j), __ldcg(sbuf + j), acc);
+                }
+                acc = lane_sum<32>(acc);
+                if (wl == 0) {
+                    const int p = i / B, c = i % B;
+                    const int sr = sr_of(r0, r1, p);
+                    const int cc = FWD ? c : B - 1 - c;
+                    const int row = a.perm ? a.perm[sr] : sr;
+                    z[static_cast<int64_t>(row) * B + cc] = acc;
+                }
             }
         }
-        grid_barrier(bar, target);
+        bar_arrive<CL>(bar);
+        // the next group's rows: everything z-independent, during the barrier
+        if (t + 1 < a.ngrp) {
+            const int4 gn = a.grp[FWD ? t + 1 : a.ngrp - 2 - t];
+            const int q = blockIdx.x + lg * gridDim.x;
+            grow_load<B, L, PF>(a, bvec, invd, z, sr_of(gn.x, gn.y, q), q < gn.y - gn.x, lane, P);
+        }
+        bar_wait<CL>(bar, target);
     }
 }
 
@@ -292,9 +384,11 @@ int sweep_grid()
     if (!g) {
         int sms = 0, occ = 0;
         ED_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        ED_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group_sweep<3, 32, true>, kGT, 0));
+        ED_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group_sweep<3, 32, true, false>, kGT, 0));
         static const int per_sm = std::getenv("ED_SWEEP_CTAS") ? std::atoi(std::getenv("ED_SWEEP_CTAS")) : 1;
         g = sms * std::max(1, std::min(occ, per_sm));
+        // ED_SWEEP_GRID=n: fewer CTAs (cheaper barrier, less bandwidth)
+        if (std::getenv("ED_SWEEP_GRID")) g = std::min(g, std::max(1, std::atoi(std::getenv("ED_SWEEP_GRID"))));
     }
     return g;
 }
@@ -308,22 +402,52 @@ int sweep_grid()
     default: { constexpr int LL = 32; __VA_ARGS__; break; } \
     }
 
+template <int B, int LL, bool FWD>
+void launch_one(const GrpArgs& a, const double* b, double* z, const double* invd, const double* X, double* sbuf,
+                unsigned int* bar, bool cluster, cudaStream_t s)
+{
+    if (!cluster) {
+        k_group_sweep<B, LL, FWD, false><<<sweep_grid(), kGT, 0, s>>>(a, b, z, invd, X, sbuf, bar);
+        return;
+    }
+    auto kern = k_group_sweep<B, LL, FWD, true>;
+    static bool attr_done[64] = {};
+    int dev = 0;
+    ED_CUDA(cudaGetDevice(&dev));
+    if (!attr_done[dev & 63]) {
+        ED_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr_done[dev & 63] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kGroupCluster, 1, 1);
+    cfg.blockDim = dim3(kGT, 1, 1);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kGroupCluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ED_CUDA(cudaLaunchKernelEx(&cfg, kern, a, b, z, invd, X, sbuf, bar));
+}
+
 template <int B>
 void launch_group(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s,
                   const double* X)
 {
     const BsrStruct& S = *A.st;
     const GrpArgs a = gargs_of(A);
-    ED_CUDA(cudaMemsetAsync(S.gbar.p, 0, sizeof(unsigned int), s));
-    const int grid = sweep_grid();
+    const bool cluster = S.grp_cluster;
+    if (!cluster) ED_CUDA(cudaMemsetAsync(S.gbar.p, 0, sizeof(unsigned int), s));
     const double* Xd = X ? X + (fwd ? 0 : S.grp_tinv) : nullptr;
     ED_GLANES(S.Ls, {
         if (fwd)
-            k_group_sweep<B, LL, true><<<grid, kGT, 0, s>>>(a, b, z, invd, Xd, S.gsbuf.p, S.gbar.p);
+            launch_one<B, LL, true>(a, b, z, invd, Xd, S.gsbuf.p, S.gbar.p, cluster, s);
         else
-            k_group_sweep<B, LL, false><<<grid, kGT, 0, s>>>(a, b, z, invd, Xd, S.gsbuf.p, S.gbar.p);
+            launch_one<B, LL, false>(a, b, z, invd, Xd, S.gsbuf.p, S.gbar.p, cluster, s);
     })
-    after_launch("k_group_sweep");
+    after_launch(cluster ? "k_group_sweep(cluster)" : "k_group_sweep");
 }
 
 } // namespace

@@ -640,7 +640,7 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
     if (S.nitems == 0) return;
     const int nlev = S.nlev();
     const BsrArgs a = args_of(A);
-    if (S.ngrp > 0 && sweep_mode() == 0) {
+    if (group_sweep_on(S)) {
         sgs_group(A, b, z, invd, fwd, s, dense);
         return;
     }
@@ -759,7 +759,7 @@ void sgs_sweep(const Bsr& A, const double* b, double* z, const double* invd, boo
     // pointers, b and inv_diag read, z read and written
     const double bytes = static_cast<double>(S.nnzb) * (8.0 * B * B + 4.0) + 4.0 * (S.nbr + 1) +
                          4.0 * 8.0 * S.nbr * B;
- const char* kname = S.ngrp > 0 && sweep_mode() == 0 ? "k_group_sweep" : S.ring_cs > 0 ? "k_sgs_push" : S.blocked ? "k_sgs_blocked" : S.cluster > 0 ? "k_sgs_cluster" : S.chain ? "k_sgs_chain"
+ const char* kname = group_sweep_on(S) ? "k_group_sweep" : S.ring_cs > 0 ? "k_sgs_push" : S.blocked ? "k_sgs_blocked" : S.cluster > 0 ? "k_sgs_cluster" : S.chain ? "k_sgs_chain"
                                                                                               : "k_sgs_flow";
     AcctScope acct(s, kname, bytes);
     if (B == 1) return launch_sgs<1>(A, b, z, invd, forward, s, dense);
@@ -769,14 +769,23 @@ void sgs_sweep(const Bsr& A, const double* b, double* z, const double* invd, boo
 
 int sweep_mode()
 {
-    // ED_SWEEP=legacy: the round-1 sweeps (dataflow / cluster push / blocked)
-    static const int mode = std::getenv("ED_SWEEP") && std::string(std::getenv("ED_SWEEP")) == "legacy" ? 1 : 0;
+    // ED_SWEEP=legacy: never the group sweep; ED_SWEEP=group: always (where a schedule exists)
+    static const int mode = !std::getenv("ED_SWEEP")                              ? 0
+                            : std::string(std::getenv("ED_SWEEP")) == "legacy" ? 1
+                            : std::string(std::getenv("ED_SWEEP")) == "group"  ? 2
+                                                                               : 0;
     return mode;
+}
+
+bool group_sweep_on(const BsrStruct& S)
+{
+    const int mode = sweep_mode();
+    return S.ngrp > 0 && mode != 1 && (mode == 2 || S.grp_use);
 }
 
 void sweep_prepare(const Bsr& A, const double* invd, DevArray<double>& aux, cudaStream_t s)
 {
-    if (A.st->ngrp > 0 && sweep_mode() == 0) return group_prepare(A, invd, aux, s);
+    if (group_sweep_on(*A.st)) return group_prepare(A, invd, aux, s);
     blocked_dense(A, aux, s);
 }
 

@@ -236,6 +236,8 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
     tail = -1;
     fallback = false;
     const double t0 = now_ms();
+    const double host0 = host_ms_acc();
+    double host_helpers = 0.0; // host work of the helper threads (level operator, dense tail)
     const bool device_ok = o.block_size == A0.st->Rb && (A0.st->Rb == 1 || A0.st->Rb == 3) &&
                            std::getenv("ED_HOST_AMG") == nullptr;
     if (device_ok) {
@@ -255,6 +257,7 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
         // 1 is never collapsed into the dense tail when it has > tail_max rows.
         std::thread lop_th;
         std::exception_ptr err_l;
+        double host_lop = 0.0;
         Bsr pre_op;
         int pre_l = -1;
         struct Joiner {
@@ -282,6 +285,7 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
                     ED_CUDA(cudaSetDevice(c.device));
                     pre_op = bsr_leveled(m, ts);
                     ED_CUDA(cudaStreamSynchronize(ts));
+                    host_lop = host_ms_acc();
                 } catch (...) {
                     err_l = std::current_exception();
                 }
@@ -290,11 +294,11 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
         DevSetupResult R = amg_build_device(A0, o, s, on_level);
         Joiner lop_joiner_r{lop_th}; // joins before R (which the thread reads) is destroyed
         lap("device setup");
-        setup_host_ms = 0.0;
         if (R.fallback) {
             fallback = true;
             fb_invd.upload(R.fallback_inv_diag, s);
             ED_CUDA(cudaStreamSynchronize(s));
+            setup_host_ms = host_ms_acc() - host0;
             return;
         }
         const int L = static_cast<int>(R.levels.size());
@@ -377,6 +381,9 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
         if (err_t) std::rethrow_exception(err_t);
         ED_CUDA(cudaStreamSynchronize(s));
         lap("dense tail");
+        if (lop_th.joinable()) lop_th.join();
+        host_helpers += host_lop;
+        setup_host_ms = host_ms_acc() - host0 + host_helpers;
         return;
     }
     const HostCsr A0h = bsr_to_csr(A0, s);
@@ -495,6 +502,7 @@ struct BlockOp final : DOp {
     int64_t size() const override { return static_cast<int64_t>(W.nv) + W.np; }
     void apply(const double* x, double* y) override
     {
+        if (W.K.n_nodes > 0) return spmv44(W.K, x, y, W.nv, W.np, s);
         spmv2(W.A, x, W.B, x + W.nv, y, 1.0, s);
         spmv2(W.C, x, W.D, x + W.nv, y + W.nv, 1.0, s);
     }

@@ -315,7 +315,21 @@ void make_work(Ctx& c, WorkSys& W, bool scale, double eps_diag)
     W.scaled = scale;
     const int nv = S.nv, np = S.np;
     W.w.alloc(static_cast<size_t>(nv) + np);
-    if (!scale) return;
+    // the coupled 4x4 operator from the assembled node blocks (scaling folded in below)
+    const bool coupled = c.sys_from_mesh && S.Bv == 3 && c.k4.p && std::getenv("ED_NO_K44") == nullptr;
+    W.K.n_nodes = 0;
+    if (coupled) {
+        W.K.n_nodes = S.D.st->nbr;
+        W.K.nnzb = S.D.st->nnzb;
+        W.K.rowptr = S.D.st->rowptr.p;
+        W.K.col = S.D.st->col.p;
+        W.K.fidx = c.d_fidx.p;
+        W.K.val.alloc(16 * static_cast<size_t>(W.K.nnzb));
+    }
+    if (!scale) {
+        if (coupled) k44_build(W.K, c.k4.p, nullptr, nv, s);
+        return;
+    }
     DevArray<double> da(nv), dd(np), mx(2);
     bsr_diag(W.A, da.p, s);
     bsr_diag(W.D, dd.p, s);
@@ -328,6 +342,7 @@ void make_work(Ctx& c, WorkSys& W, bool scale, double eps_diag)
     bsr_scale(W.B, wv, wp, s);
     bsr_scale(W.C, wp, wv, s);
     bsr_scale(W.D, wp, wp, s);
+    if (coupled) k44_build(W.K, c.k4.p, W.w.p, nv, s);
     ED_CUDA(cudaStreamSynchronize(s)); // temporaries die here
 }
 

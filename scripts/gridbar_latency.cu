@@ -17,6 +17,54 @@ __device__ __forceinline__ void red_rel(unsigned* p, unsigned v)
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ unsigned atom_add_rel(unsigned* p, unsigned v)
+{
+    unsigned old;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned ld_rlx(const unsigned* p)
+{
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_rel(unsigned* p, unsigned v)
+{
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// flag barrier: arrivals count on ctr; the last arriver publishes the generation on flag (another line)
+__global__ void k_bar2(unsigned* ctr, int nbar, double* buf, int work, int relaxed_poll)
+{
+    const unsigned G = gridDim.x;
+    unsigned* flag = ctr + 32;
+    double acc = 0.0;
+    for (int b = 0; b < nbar; ++b) {
+        if (work && threadIdx.x < 32) {
+            const int src = (blockIdx.x + 7 * b + threadIdx.x) % G;
+            acc += __ldcg(buf + src * 32 + threadIdx.x);
+            buf[blockIdx.x * 32 + threadIdx.x] = acc;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned old = atom_add_rel(ctr, 1u);
+            if (old == G * (b + 1) - 1) {
+                st_rel(flag, b + 1);
+            } else if (relaxed_poll) {
+                while (ld_rlx(flag) < static_cast<unsigned>(b + 1)) {
+                }
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            } else {
+                while (ld_acq(flag) < static_cast<unsigned>(b + 1)) {
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (acc == 12345.0) buf[0] = acc;
+}
+
 __global__ void k_bar(unsigned* ctr, int nbar, double* buf, int work)
 {
     const unsigned G = gridDim.x;
@@ -44,7 +92,7 @@ int main()
 {
     unsigned* ctr;
     double* buf;
-    cudaMalloc(&ctr, 4);
+    cudaMalloc(&ctr, 4 * 64);
     cudaMalloc(&buf, 8 * 32 * 4096);
     cudaMemset(buf, 0, 8 * 32 * 4096);
     cudaEvent_t a, b;
@@ -67,6 +115,26 @@ int main()
                     if (ms < best) best = ms;
                 }
                 printf("CTAs %4d threads %3d work %d: %.3f us per barrier\n", G, threads, work, best * 1e3 / nbar);
+            }
+        }
+    }
+    for (int relaxed : {0, 1}) {
+        for (int per_sm : {1, 2}) {
+            for (int work : {0, 1}) {
+                const int G = 148 * per_sm;
+                float best = 1e9;
+                for (int rep = 0; rep < 5; ++rep) {
+                    cudaMemset(ctr, 0, 4 * 64);
+                    cudaEventRecord(a);
+                    k_bar2<<<G, 256>>>(ctr, nbar, buf, work, relaxed);
+                    cudaEventRecord(b);
+                    cudaEventSynchronize(b);
+                    float ms;
+                    cudaEventElapsedTime(&ms, a, b);
+                    if (ms < best) best = ms;
+                }
+                printf("flag barrier (%s poll) CTAs %4d work %d: %.3f us per barrier\n", relaxed ? "relaxed" : "acquire", G,
+                       work, best * 1e3 / nbar);
             }
         }
     }
