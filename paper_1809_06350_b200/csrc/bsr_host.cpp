@@ -48,7 +48,7 @@ void gs_level_order(const BlockPattern& pat, std::vector<int>& order, std::vecto
 namespace {
 constexpr int kRingSliceMaxBytes = 40 * 1024; // z slice per CTA (b and inv_diag slices alongside)
 constexpr int kRingPartMaxBytes = 24 * 1024;  // one partial-sum slot per CTA
-constexpr int kRingMinRows = 4096;            // smaller operators: blocked sweep / dense tail
+constexpr int kRingMinRows = 4096;            // smaller operators: group / chain sweeps, dense tail
 
 int64_t push_chunk_bytes(int64_t m, int64_t pk0, int64_t pk1, int64_t s0, int64_t nown, int B)
 {
@@ -384,91 +384,9 @@ std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLay
     int widest = 0;
     for (int l = 0; l < nlev; ++l) widest = std::max(widest, S.lev_ptr[l + 1] - S.lev_ptr[l]);
     S.chain = static_cast<int64_t>(widest) * S.Ls <= 1024;
-    // narrow, deep schedules whose vector fits in a cluster's shared memory
-    // (<= 16 CTAs x 192 KB) run cluster-resident: z lives in DSMEM and a
-    // cluster barrier separates levels
     S.avg_rows_per_level = nlev > 0 ? S.nbr / nlev : 0;
-    const int64_t zbytes = static_cast<int64_t>(S.nbr) * Rb * 8;
-    S.cluster = 0;
-    static const int max_rpl = std::getenv("ED_CLUSTER_MAX_RPL") ? std::atoi(std::getenv("ED_CLUSTER_MAX_RPL")) : 32;
-    if (Rb == Cb && nlev > 1 && S.avg_rows_per_level <= max_rpl && std::getenv("ED_NO_CLUSTER") == nullptr) {
-        for (int cs = 1; cs <= 16; cs *= 2)
-            if (zbytes <= static_cast<int64_t>(cs) * 192 * 1024) {
-                S.cluster = cs;
-                break;
-            }
-        // enough lanes that a level's blocks spread to <= ~4 per thread
-        const double blocks_per_level = static_cast<double>(S.nnzb) / nlev;
-        while (S.cluster > 0 && S.cluster < 16 && blocks_per_level > 4.0 * 512 * S.cluster) S.cluster *= 2;
-    }
-    // blocked sweep: narrow schedules (fewer groups than ~1.5x levels) whose z
-    // fits one CTA's shared memory
-    const int GR = 32 / Rb;
-    const int ng = (n + GR - 1) / GR;
-    if (Rb == Cb && (Rb == 1 || Rb == 3) && nlev > 1 && static_cast<int64_t>(n) * Rb <= BsrStruct::kBlockedMaxScalars &&
-        2 * static_cast<int64_t>(ng) <= 3 * static_cast<int64_t>(nlev) && std::getenv("ED_NO_BLOCKED") == nullptr) {
-        S.blocked = true;
-        S.ngroups = ng;
-        std::vector<int> colp(S.nnzb);
-        std::vector<int> imap(static_cast<size_t>(ng) * 3 * 1024, -1);
-        for (int s2 = 0; s2 < n; ++s2) {
-            const int g = s2 / GR, lr = s2 - g * GR;
-            for (int k = S.h_rowptr[s2]; k < S.h_rowptr[s2 + 1]; ++k) {
-                const int sc = identity ? S.h_col[k] : lay.inv[S.h_col[k]];
-                colp[k] = sc;
-                const int gc = sc / GR, lc = sc - gc * GR;
-                const int which = gc == g ? 0 : gc == g - 1 ? 1 : gc == g + 1 ? 2 : -1;
-                if (which < 0) continue;
-                int* M = imap.data() + (static_cast<size_t>(g) * 3 + which) * 1024;
-                for (int r = 0; r < Rb; ++r)
-                    for (int d = 0; d < Cb; ++d) M[(lc * Rb + d) * 32 + lr * Rb + r] = k * Rb * Cb + r * Cb + d;
-            }
-        }
-        S.colp.upload(colp, s);
-        S.imap.upload(imap, s);
-        // producer units: (row, chunk of <= 32*U blocks), U blocks per lane in flight
-        int chunk = 32 * (Rb == 3 ? 2 : 8); // kernels_blocked.cu: kU3 / kU1 blocks per lane
-        for (;;) {
-            int worst = 0;
-            for (int g = 0; g < ng; ++g) {
-                int u = 0;
-                for (int s2 = g * GR; s2 < std::min(n, (g + 1) * GR); ++s2)
-                    u += std::max(1, (S.h_rowptr[s2 + 1] - S.h_rowptr[s2] + chunk - 1) / chunk);
-                worst = std::max(worst, u);
-            }
-            if (worst <= BsrStruct::kBlockedMaxUnits) {
-                S.max_units = worst;
-                break;
-            }
-            chunk *= 2;
-        }
-        std::vector<int> gunit{0}, rowu(static_cast<size_t>(ng) * 33, 0);
-        std::vector<int4> units;
-        for (int g = 0; g < ng; ++g) {
-            const int base = static_cast<int>(units.size());
-            int lr = 0;
-            for (int s2 = g * GR; s2 < std::min(n, (g + 1) * GR); ++s2, ++lr) {
-                const int first = static_cast<int>(units.size()) - base;
-                rowu[static_cast<size_t>(g) * 33 + lr] = first;
-                const int kb = S.h_rowptr[s2], ke = S.h_rowptr[s2 + 1];
-                int k0 = kb;
-                do {
-                    const int k1 = std::min(ke, k0 + chunk);
-                    units.push_back(make_int4(lr, k0, k1, first));
-                    k0 = k1;
-                } while (k0 < ke);
-            }
-            for (; lr <= 32; ++lr) rowu[static_cast<size_t>(g) * 33 + lr] = static_cast<int>(units.size()) - base;
-            gunit.push_back(static_cast<int>(units.size()));
-        }
-        S.gunit.upload(gunit, s);
-        S.units.upload(units, s);
-        S.rowu.upload(rowu, s);
-    }
     if (lay.ring_cs > 0 && Rb == Cb && pat.nbr == pat.nbc) {
         ring_build(S, lay, s);
-        S.blocked = false;
-        S.cluster = 0;
     }
     if (Rb == Cb && (Rb == 1 || Rb == 3) && pat.nbr == pat.nbc && S.leveled && S.nbr > 0) group_build(S, s);
     ED_CUDA(cudaStreamSynchronize(s)); // host vectors die at return

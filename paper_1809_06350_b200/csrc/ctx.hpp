@@ -86,7 +86,7 @@ struct DevLevel {
     const Bsr* A = nullptr; // level operator (fine: borrowed)
     Bsr Aown, P, R;
     DevArray<double> invd, r, z, s; // r/z for coarse levels, s scratch
-    DevArray<double> gdense;         // blocked Gauss-Seidel group blocks (A->st->blocked)
+    DevArray<double> gdense;         // sweep auxiliary data (sweep_prepare: group T^-1 / push packed blocks)
     int n = 0;
 };
 struct DevHierarchy {

@@ -184,23 +184,8 @@ struct BsrStruct {
     DevArray<int> lev_items;  // [nlev] items per level
     DevArray<unsigned int> sync; // [nlev + 2]: per-level done counters, ticket
     bool chain = false;          // narrow levels: single-CTA sweep with CTA barriers
-    int cluster = 0;             // > 0: cluster-resident sweep over this many CTAs (z in DSMEM)
     int avg_rows_per_level = 0;
     DevArray<int> d_lev_ptr;     // device copy of lev_ptr
-    // blocked sweep (narrow schedules whose z fits one CTA's shared memory):
-    // groups of 32/Rb consecutive stored rows; one warp solves a group's
-    // scalar rows in sweep order while the other warps sum the next group's
-    // rows over everything outside it (kernels_sparse.cu: k_sgs_blocked)
-    bool blocked = false;
-    int ngroups = 0;
-    DevArray<int> colp; // [nnzb] stored position of each block's column
-    DevArray<int> imap; // [ngroups][3][32*32] value index of the group's own / previous / next block, col-major, -1: 0
-    DevArray<int> gunit;  // [ngroups+1] first unit of each group
-    DevArray<int4> units; // (local row, k0, k1, first unit of the row) row-chunk units of the producers' sums
-    DevArray<int> rowu;   // [ngroups][33] first unit of each local row (relative to the group), last = count
-    int max_units = 0;    // per group
-    static constexpr int kBlockedMaxScalars = 20480;
-    static constexpr int kBlockedMaxUnits = 1024;
     // cluster push sweep (kernels_ring.cu): rows of each level dealt to
     // ring_cs CTAs, which own their z; CTA c computes, for every row of a
     // level, the partial row sum over the columns it owns and pushes it to the
@@ -314,22 +299,16 @@ void spmv(const Bsr& M, const double* x, double* y, const double* b, int mode, c
 void spmv2(const Bsr& M1, const double* x1, const Bsr& M2, const double* x2, double* y, double sgn,
            cudaStream_t s);
 // one in-place Gauss-Seidel half sweep over the level schedule (dataflow kernel)
-// dense: the operator's group blocks (blocked_dense) when A.st->blocked
+// dense: the operator's sweep auxiliary data (sweep_prepare)
 void sgs_sweep(const Bsr& A, const double* b, double* z, const double* inv_diag, bool forward,
                cudaStream_t s, const double* dense = nullptr);
-// sweep auxiliary data (values as of the call): own / previous / next group
-// blocks of a blocked-sweep operator, packed blocks of a push-sweep operator
-void blocked_dense(const Bsr& A, DevArray<double>& dense, cudaStream_t s);
-// blocked half sweep (kernels_blocked.cu), A.st->blocked
-void sgs_blocked(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s,
-                 const double* dense);
 // ED_SWEEP: 0 default (group sweep where BsrStruct::grp_use), 1 legacy, 2 group everywhere
 int sweep_mode();
 bool group_sweep_on(const BsrStruct& S);
 // per-value-change auxiliary data of a Gauss-Seidel operator: the group
-// sweep's T^-1 (or the legacy sweeps' packed / group blocks)
+// sweep's T^-1, or the push sweep's packed blocks (none for the dataflow / chain sweeps)
 void sweep_prepare(const Bsr& A, const double* invd, DevArray<double>& aux, cudaStream_t s);
-// level-group half sweep (kernels_group.cu), A.st->ngrp > 0; X = group_prepare output
+// level-group half sweep (kernels_group.cu); X = group_prepare output
 void sgs_group(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s,
                const double* X);
 // packed in-group triangular inverses of both sweep directions (values and inv_diag as of the call)

@@ -273,8 +273,7 @@ __global__ void __launch_bounds__(kThreads) k_sgs_flow(BsrArgs m, const double* 
                                                        const double* __restrict__ invd, int nitems, int nlev,
                                                        const int* __restrict__ item_row,
                                                        const int* __restrict__ item_level,
-                                                       const int* __restrict__ lev_items, unsigned int* sync,
-                                                       unsigned long long* trace)
+                                                       const int* __restrict__ lev_items, unsigned int* sync)
 {
     // enough blocks per lane prefetched that no column index is loaded after the wait
     constexpr int PF = (B == 3) ? 3 : 4;
@@ -290,7 +289,6 @@ __global__ void __launch_bounds__(kThreads) k_sgs_flow(BsrArgs m, const double* 
         __syncthreads();
         if (t >= nitems) return;
         const int item = FWD ? t : nitems - 1 - t;
-        if (trace && threadIdx.x == 0) trace[item * 3 + 0] = globaltimer();
         const int lev = item_level[item];
         const int s = item_row[item] + g;
         const bool valid = s < item_row[item + 1];
@@ -307,206 +305,12 @@ __global__ void __launch_bounds__(kThreads) k_sgs_flow(BsrArgs m, const double* 
             }
             __syncthreads();
         }
-        if (trace && threadIdx.x == 0) trace[item * 3 + 1] = globaltimer();
         finish_row<B, L, PF, FWD, true>(m, z, valid, lane, P);
         __syncthreads();
-        if (trace && threadIdx.x == 0) trace[item * 3 + 2] = globaltimer();
         if (threadIdx.x == 0) red_release_add(done + lev, 1u); // publishes the CTA's z writes (bar.sync + release)
     }
 }
 
-constexpr int kClT = 512;
-constexpr int kPFB = 3; // blocks per lane prefetched ahead of the level barrier
-
-template <int B>
-struct ClRow {
-    int s, row, kb, ke, lane, G;
-    bool valid;
-    int c[kPFB];
-    double v[kPFB][B * B];
-    double bb[B], id[B], D[B * B];
-};
-
-// Rows of level `lev` dealt to this CTA: q = q0 + tid / G (q < myR).  Loads
-// everything that does not depend on z: the lane's first kPFB blocks, and for
-// the group leader b, inv_diag and the diagonal block.
-template <int B>
-__device__ __forceinline__ void cl_prefetch(const BsrArgs& m, const double* __restrict__ bvec,
-                                            const double* __restrict__ invd, const int* __restrict__ lev_ptr, int lev,
-                                            int rank, int cs, int tid, int q0, ClRow<B>& P)
-{
-    const int r0 = lev_ptr[lev], R = lev_ptr[lev + 1] - r0;
-    const int myR = R > rank ? (R - rank + cs - 1) / cs : 0;
-    int G = kClT;
-    while (G > 1 && G * myR > kClT) G >>= 1;
-    P.G = G;
-    const int q = q0 + tid / G;
-    P.lane = tid % G;
-    P.valid = q < myR;
-    P.s = r0 + rank + q * cs;
-    P.row = P.valid ? (m.perm ? m.perm[P.s] : P.s) : 0;
-    P.kb = P.valid ? m.rowptr[P.s] + P.lane : 0;
-    P.ke = P.valid ? m.rowptr[P.s + 1] : 0;
-#pragma unroll
-    for (int j = 0; j < kPFB; ++j) {
-        const int k = P.kb + j * G;
-        P.c[j] = k < P.ke ? __ldg(m.col + k) : -1;
-        if (k < P.ke) {
-#pragma unroll
-            for (int e = 0; e < B * B; ++e) P.v[j][e] = __ldg(m.val + static_cast<int64_t>(k) * (B * B) + e);
-        }
-    }
-    if (P.valid && P.lane == 0) {
-        const int dp = m.dpos[P.s];
-#pragma unroll
-        for (int d = 0; d < B; ++d) {
-            P.bb[d] = bvec[static_cast<int64_t>(P.row) * B + d];
-            P.id[d] = invd[static_cast<int64_t>(P.row) * B + d];
-        }
-#pragma unroll
-        for (int e = 0; e < B * B; ++e) P.D[e] = dp >= 0 ? __ldg(m.val + static_cast<int64_t>(dp) * (B * B) + e) : 0.0;
-    }
-}
-
-// Gauss-Seidel half sweep over narrow, deep schedules with z resident in
-// the cluster's distributed shared memory: each CTA holds a slice of z; the
-// rows of a level are dealt round-robin to the CTAs, each row gets G lanes (a
-// power of two sized so the level fills the CTA), lanes gather z through
-// DSMEM, the group leader solves the diagonal block in sweep order and writes
-// the new values to the owning slice (and to global memory); a cluster
-// barrier (release/acquire) separates levels.  The next level's matrix data
-// is loaded before the barrier, so only DSMEM gathers sit on the critical
-// path of a level.
-__device__ __forceinline__ void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
-__device__ __forceinline__ void cluster_wait_acquire() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
-__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
-
-template <int B, bool FWD, bool MULTI>
-__global__ void __launch_bounds__(kClT) k_sgs_cluster(BsrArgs m, const double* __restrict__ bvec, double* z,
-                                                      const double* __restrict__ invd,
-                                                      const int* __restrict__ lev_ptr, int nlev, int nsc, int slice)
-{
-    extern __shared__ double smem[];
-    double* zs = smem;          // this CTA's slice of z
-    double* red = smem + slice; // [kClT/32][B] cross-warp partials
-    cg::cluster_group cl = cg::this_cluster();
-    const int rank = static_cast<int>(cl.block_rank());
-    const int cs = static_cast<int>(cl.num_blocks());
-    const int tid = threadIdx.x;
-    for (int i = tid; i < slice; i += kClT) {
-        const int gi = rank * slice + i;
-        zs[i] = gi < nsc ? z[gi] : 0.0;
-    }
-    auto zptr = [&](int gi) -> double* {
-        if (!MULTI) return zs + gi;
-        const int owner = gi / slice;
-        return cl.map_shared_rank(zs, owner) + (gi - owner * slice);
-    };
-    ClRow<B> P;
-    cl_prefetch<B>(m, bvec, invd, lev_ptr, FWD ? 0 : nlev - 1, rank, cs, tid, 0, P);
-    if (MULTI) cl.sync();
-    else __syncthreads();
-    for (int li = 0; li < nlev; ++li) {
-        const int lev = FWD ? li : nlev - 1 - li;
-        const int R = lev_ptr[lev + 1] - lev_ptr[lev];
-        const int myR = R > rank ? (R - rank + cs - 1) / cs : 0;
-        const int rpp = kClT / P.G;
-        for (int q0 = 0; q0 < myR; q0 += rpp) {
-            if (q0 > 0) cl_prefetch<B>(m, bvec, invd, lev_ptr, lev, rank, cs, tid, q0, P);
-            const int G = P.G;
-            double acc[B];
-#pragma unroll
-            for (int r = 0; r < B; ++r) acc[r] = 0.0;
-            {
-                double zv[kPFB][B];
-#pragma unroll
-                for (int j = 0; j < kPFB; ++j) {
-                    const int cc = P.c[j] >= 0 ? P.c[j] : 0;
-#pragma unroll
-                    for (int d = 0; d < B; ++d) zv[j][d] = *zptr(cc * B + d);
-                }
-#pragma unroll
-                for (int j = 0; j < kPFB; ++j) {
-                    const bool use = P.c[j] >= 0 && P.c[j] != P.row;
-#pragma unroll
-                    for (int d = 0; d < B; ++d)
-#pragma unroll
-                        for (int r = 0; r < B; ++r) acc[r] = use ? fma(P.v[j][r * B + d], zv[j][d], acc[r]) : acc[r];
-                }
-            }
-            for (int k = P.kb + kPFB * G; k < P.ke; k += G) {
-                const int c = __ldg(m.col + k);
-                if (c == P.row) continue;
-                const double* vp = m.val + static_cast<int64_t>(k) * (B * B);
-#pragma unroll
-                for (int d = 0; d < B; ++d) {
-                    const double zv = *zptr(c * B + d);
-#pragma unroll
-                    for (int r = 0; r < B; ++r) acc[r] = fma(__ldg(vp + r * B + d), zv, acc[r]);
-                }
-            }
-            if (G <= 32) {
-#pragma unroll
-                for (int r = 0; r < B; ++r)
-                    for (int o = G / 2; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o, G);
-            } else {
-#pragma unroll
-                for (int r = 0; r < B; ++r)
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
-                if ((tid & 31) == 0)
-#pragma unroll
-                    for (int r = 0; r < B; ++r) red[(tid >> 5) * B + r] = acc[r];
-                __syncthreads();
-                if (P.lane == 0) {
-                    const int w0 = tid >> 5;
-#pragma unroll
-                    for (int r = 0; r < B; ++r) {
-                        double t = 0.0;
-                        for (int ww = 0; ww < G / 32; ++ww) t += red[(w0 + ww) * B + r];
-                        acc[r] = t;
-                    }
-                }
-                __syncthreads();
-            }
-            if (P.valid && P.lane == 0) {
-                double zv[B];
-#pragma unroll
-                for (int d = 0; d < B; ++d) zv[d] = *zptr(P.row * B + d);
-#pragma unroll
-                for (int ci = 0; ci < B; ++ci) {
-                    const int c = FWD ? ci : B - 1 - ci;
-                    double a = P.bb[c] - acc[c];
-#pragma unroll
-                    for (int d = 0; d < B; ++d)
-                        if (d != c) a -= P.D[c * B + d] * zv[d];
-                    zv[c] = a * P.id[c];
-                }
-#pragma unroll
-                for (int d = 0; d < B; ++d) *zptr(P.row * B + d) = zv[d];
-                if (MULTI) fence_cluster(); // only writers pay the release fence
-            }
-        }
-        if (MULTI) {
-            cluster_arrive_relaxed();
-            if (li + 1 < nlev) cl_prefetch<B>(m, bvec, invd, lev_ptr, FWD ? li + 1 : nlev - 2 - li, rank, cs, tid, 0, P);
-            cluster_wait_acquire();
-        } else {
-            if (li + 1 < nlev) cl_prefetch<B>(m, bvec, invd, lev_ptr, FWD ? li + 1 : nlev - 2 - li, rank, cs, tid, 0, P);
-            __syncthreads();
-        }
-    }
-    // slices back to global memory
-    for (int i = tid; i < slice; i += kClT) {
-        const int gi = rank * slice + i;
-        if (gi < nsc) z[gi] = zs[i];
-    }
-    if (MULTI) cl.sync(); // keep remote slices alive until every CTA is done
-}
-
-
-// One Gauss-Seidel half sweep over narrow levels: a single CTA walks the
-// levels with a CTA barrier between them (no global atomics or polling).
 template <int B, int L, bool FWD>
 __global__ void __launch_bounds__(512) k_sgs_chain(BsrArgs m, const double* __restrict__ bvec, double* z,
                                                     const double* __restrict__ invd, const int* __restrict__ lev_ptr,
@@ -648,40 +452,6 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
         sgs_ring(A, b, z, invd, fwd, s, dense);
         return;
     }
-    if (S.blocked) {
-        sgs_blocked(A, b, z, invd, fwd, s, dense);
-        return;
-    }
-    if (S.cluster > 0) {
-        const int nsc = S.nbr * B;
-        const int cs = S.cluster;
-        const int slice = (nsc + cs - 1) / cs;
-        const size_t smem = (static_cast<size_t>(slice) + (kClT / 32) * B) * sizeof(double);
-        auto kern = cs > 1 ? (fwd ? k_sgs_cluster<B, true, true> : k_sgs_cluster<B, false, true>)
-                           : (fwd ? k_sgs_cluster<B, true, false> : k_sgs_cluster<B, false, false>);
-        static bool attr_done[2][2][2] = {};
-        bool& done = attr_done[B == 3][fwd ? 1 : 0][cs > 1 ? 1 : 0];
-        if (!done) {
-            ED_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            ED_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            done = true;
-        }
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(cs, 1, 1);
-        cfg.blockDim = dim3(kClT, 1, 1);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = cs;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        ED_CUDA(cudaLaunchKernelEx(&cfg, kern, a, b, z, invd, S.d_lev_ptr.p, nlev, nsc, slice));
-        after_launch("k_sgs_cluster");
-        return;
-    }
     if (S.chain) {
         ED_LANES(S.Ls, {
             if (fwd)
@@ -694,32 +464,15 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
     }
     ED_CUDA(cudaMemsetAsync(S.sync.p, 0, S.sync.n * sizeof(unsigned int), s));
     const int grid = std::min(S.nitems, 148 * 2);
-    // ED_FLOW_TRACE=<nitems>: dump per-item timestamps of the first forward sweep with that many items
-    static const int trace_n = std::getenv("ED_FLOW_TRACE") ? std::atoi(std::getenv("ED_FLOW_TRACE")) : -1;
-    static bool traced = false;
-    unsigned long long* tr = nullptr;
-    if (!traced && fwd && nlev == trace_n) ED_CUDA(cudaMallocManaged(&tr, sizeof(unsigned long long) * 3 * S.nitems));
     ED_LANES(S.Ls, {
         if (fwd)
             k_sgs_flow<B, LL, true><<<grid, kThreads, 0, s>>>(a, b, z, invd, S.nitems, nlev, S.item_row.p,
-                                                             S.item_level.p, S.lev_items.p, S.sync.p, tr);
+                                                             S.item_level.p, S.lev_items.p, S.sync.p);
         else
             k_sgs_flow<B, LL, false><<<grid, kThreads, 0, s>>>(a, b, z, invd, S.nitems, nlev, S.item_row.p,
-                                                              S.item_level.p, S.lev_items.p, S.sync.p, tr);
+                                                              S.item_level.p, S.lev_items.p, S.sync.p);
     })
     after_launch("k_sgs_flow");
-    if (tr) {
-        traced = true;
-        ED_CUDA(cudaStreamSynchronize(s));
-        std::vector<int> il(S.nitems);
-        ED_CUDA(cudaMemcpy(il.data(), S.item_level.p, sizeof(int) * S.nitems, cudaMemcpyDeviceToHost));
-        FILE* f = std::fopen("gpurun_out/flow_trace.txt", "w");
-        if (f) {
-            for (int i = 0; i < S.nitems; ++i) std::fprintf(f, "%d %d %llu %llu %llu\n", i, il[i], tr[3 * i], tr[3 * i + 1], tr[3 * i + 2]);
-            std::fclose(f);
-        }
-        cudaFree(tr);
-    }
 }
 
 } // namespace
@@ -759,7 +512,7 @@ void sgs_sweep(const Bsr& A, const double* b, double* z, const double* invd, boo
     // pointers, b and inv_diag read, z read and written
     const double bytes = static_cast<double>(S.nnzb) * (8.0 * B * B + 4.0) + 4.0 * (S.nbr + 1) +
                          4.0 * 8.0 * S.nbr * B;
- const char* kname = group_sweep_on(S) ? "k_group_sweep" : S.ring_cs > 0 ? "k_sgs_push" : S.blocked ? "k_sgs_blocked" : S.cluster > 0 ? "k_sgs_cluster" : S.chain ? "k_sgs_chain"
+ const char* kname = group_sweep_on(S) ? "k_group_sweep" : S.ring_cs > 0 ? "k_sgs_push" : S.chain ? "k_sgs_chain"
                                                                                               : "k_sgs_flow";
     AcctScope acct(s, kname, bytes);
     if (B == 1) return launch_sgs<1>(A, b, z, invd, forward, s, dense);
@@ -786,7 +539,8 @@ bool group_sweep_on(const BsrStruct& S)
 void sweep_prepare(const Bsr& A, const double* invd, DevArray<double>& aux, cudaStream_t s)
 {
     if (group_sweep_on(*A.st)) return group_prepare(A, invd, aux, s);
-    blocked_dense(A, aux, s);
+    if (A.st->ring_cs > 0) return ring_pack(A, aux, s); // push sweep: packed blocks (kernels_ring.cu)
+    aux.release();
 }
 
 void jacobi_update(double* z, const double* b, const double* t, const double* invd, double w, int64_t n,
