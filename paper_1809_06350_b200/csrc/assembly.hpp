@@ -33,6 +33,9 @@ void launch_traction(const int64_t* rowptr, const int* rows, const double* vals,
 // FP64 FMA probe: returns the flops of one launch
 double launch_fp64_fma(double* out, int iters, cudaStream_t s);
 void launch_k4_to_plane(int plane, const int* src, const double* k4, double* val, int64_t nnzb, cudaStream_t s);
+// all four planes from K4 in one pass (dst*: stored block of each K4 slot per plane, -1 none)
+void launch_k4_split(const double* k4, const int* dstA, const int* dstB, const int* dstC, const int* dstD, double* A,
+                     double* B, double* C, double* D, int64_t nslots, cudaStream_t s);
 
 // ---- system kernels (kernels_system.cu) ----
 // max |x_i| over [0, n) into *out (deterministic)

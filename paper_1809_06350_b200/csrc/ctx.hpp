@@ -156,6 +156,7 @@ struct Ctx {
     std::vector<int> color_ptr;
     DevArray<double> k4;
     DevArray<int> srcA, srcB, srcC, srcD;
+    DevArray<int> dstA, dstB, dstC, dstD; // inverse maps: stored block of each K4 slot per plane (-1: none)
     ed_material mat{};
     double body_force[3] = {0.0, 0.0, 0.0};
     DevArray<int64_t> tr_rowptr;

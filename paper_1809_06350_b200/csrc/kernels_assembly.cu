@@ -596,7 +596,52 @@ __global__ void k_k4_to_plane(const int* __restrict__ src, const double* __restr
     }
 }
 
+// All four planes from the K4 node blocks in ONE pass: a thread per node-graph
+// slot reads its 128-B block once (8 x 16-B loads) and writes the A (3x3), B
+// (3x1), C (1x3) and D (1x1) parts where they are stored (dst* = -1: the slot
+// has no block in that plane -- a fixed row or column node).
+__global__ void k_k4_split(const double* __restrict__ k4, const int* __restrict__ dstA, const int* __restrict__ dstB,
+                           const int* __restrict__ dstC, const int* __restrict__ dstD, double* __restrict__ A,
+                           double* __restrict__ B, double* __restrict__ C, double* __restrict__ D, int64_t nslots)
+{
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= nslots) return;
+    const double2* src = reinterpret_cast<const double2*>(k4 + 16 * k);
+    double K[16];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const double2 v = __ldg(src + q);
+        K[2 * q] = v.x;
+        K[2 * q + 1] = v.y;
+    }
+    const int a = dstA[k], b = dstB[k], c = dstC[k], d = dstD[k];
+    if (a >= 0) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) A[9 * static_cast<int64_t>(a) + 3 * i + j] = K[4 * i + j];
+    }
+    if (b >= 0) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) B[3 * static_cast<int64_t>(b) + i] = K[4 * i + 3];
+    }
+    if (c >= 0) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) C[3 * static_cast<int64_t>(c) + j] = K[12 + j];
+    }
+    if (d >= 0) D[d] = K[15];
+}
+
 } // namespace
+
+void launch_k4_split(const double* k4, const int* dstA, const int* dstB, const int* dstC, const int* dstD, double* A,
+                     double* B, double* C, double* D, int64_t nslots, cudaStream_t s)
+{
+    if (nslots == 0) return;
+    k_k4_split<<<static_cast<unsigned>((nslots + 255) / 256), 256, 0, s>>>(k4, dstA, dstB, dstC, dstD, A, B, C, D,
+                                                                          nslots);
+    after_launch("k_k4_split");
+}
 
 // resident CTAs per SM the element kernels are compiled for (register cap);
 // ED_ASM_MINB=<residual><tangent> picks a variant (experiments), e.g. 86

@@ -386,6 +386,14 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
         setup_host_ms = host_ms_acc() - host0 + host_helpers;
         return;
     }
+    // The host restatement (amg_host.cpp) builds the same hierarchy on the CPU.
+    // It is a parity / diagnostic path only (ED_HOST_AMG=1), never a silent
+    // fallback: an AMG block size the device setup does not handle is refused.
+    if (std::getenv("ED_HOST_AMG") == nullptr)
+        throw Error(ED_UNSUPPORTED, "AMG setup: block_size " + std::to_string(o.block_size) +
+                                        " on a " + std::to_string(A0.st->Rb) + "x" + std::to_string(A0.st->Rb) +
+                                        "-block operator is not supported on the device (block size must equal the "
+                                        "operator's block, 1 or 3)");
     const HostCsr A0h = bsr_to_csr(A0, s);
     const HostHierarchy hh = amg_build_host(A0h, o);
     setup_host_ms = now_ms() - t0;

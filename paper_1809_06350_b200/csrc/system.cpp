@@ -257,6 +257,16 @@ void ctx_build_mesh_system(Ctx& c)
     stored_src(S.lB, srcB, c.srcB);
     stored_src(S.lC, srcC, c.srcC);
     stored_src(S.lD, srcD, c.srcD);
+    auto slot_dst = [&](const BsrLayout& L, const std::vector<int64_t>& src, DevArray<int>& out) {
+        std::vector<int> v(PN.nnzb(), -1);
+        for (size_t k = 0; k < src.size(); ++k) v[src[k]] = static_cast<int>(L.addr[k]);
+        out.upload(v, s);
+        ED_CUDA(cudaStreamSynchronize(s));
+    };
+    slot_dst(S.lA, srcA, c.dstA);
+    slot_dst(S.lB, srcB, c.dstB);
+    slot_dst(S.lC, srcC, c.dstC);
+    slot_dst(S.lD, srcD, c.dstD);
     c.sys_from_mesh = true;
     c.sys_values = false;
     ED_CUDA(cudaStreamSynchronize(s));
@@ -266,10 +276,8 @@ void ctx_planes_from_k4(Ctx& c)
 {
     BlockSys& S = c.sys;
     cudaStream_t s = c.stream;
-    launch_k4_to_plane(0, c.srcA.p, c.k4.p, S.A.val.p, S.A.st->nnzb, s);
-    launch_k4_to_plane(1, c.srcB.p, c.k4.p, S.B.val.p, S.B.st->nnzb, s);
-    launch_k4_to_plane(2, c.srcC.p, c.k4.p, S.C.val.p, S.C.st->nnzb, s);
-    launch_k4_to_plane(3, c.srcD.p, c.k4.p, S.D.val.p, S.D.st->nnzb, s);
+    launch_k4_split(c.k4.p, c.dstA.p, c.dstB.p, c.dstC.p, c.dstD.p, S.A.val.p, S.B.val.p, S.C.val.p, S.D.val.p,
+                    S.D.st->nnzb, s);
     c.sys_values = true;
 }
 
