@@ -157,6 +157,7 @@ struct Ctx {
     DevArray<double> k4;
     DevArray<int> srcA, srcB, srcC, srcD;
     DevArray<int> dstA, dstB, dstC, dstD; // inverse maps: stored block of each K4 slot per plane (-1: none)
+    DevArray<int2> k44_cf;                // per node-graph block {column node, its free index} (coupled SpMV)
     ed_material mat{};
     double body_force[3] = {0.0, 0.0, 0.0};
     DevArray<int64_t> tr_rowptr;

@@ -247,6 +247,7 @@ struct CoupledOp {
     const int* rowptr = nullptr; // [n_nodes + 1] (the D plane's)
     const int* col = nullptr;    // [nnzb]
     const int* fidx = nullptr;   // node -> free velocity index (-1: fixed)
+    const int2* cf = nullptr;    // [nnzb] {column node, its free velocity index}
     DevArray<double> val;        // [nnzb][16]
     // algorithmic bytes of one y = K x: blocks + one index, row pointers, x and y
     double bytes(int64_t n_unknowns) const

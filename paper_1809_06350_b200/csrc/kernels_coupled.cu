@@ -56,9 +56,11 @@ __global__ void k_k44_build(const int* __restrict__ rowptr, const int* __restric
 }
 
 // y = K x, x = [x_v (free velocity dofs); x_p (nodes)].  L lanes per node row,
-// each lane whole 128-B blocks (8 x LDG.128).
-template <int L>
-__global__ void __launch_bounds__(kCT) k_spmv44(const int* __restrict__ rowptr, const int* __restrict__ col,
+// each lane whole 128-B blocks (8 x LDG.128); a block's column comes with its
+// free velocity index (int2 {node, free index}), so the x gathers wait on one
+// load only; PB blocks per lane are in flight at once.
+template <int L, int PB>
+__global__ void __launch_bounds__(kCT) k_spmv44(const int* __restrict__ rowptr, const int2* __restrict__ cf,
                                                 int n_nodes, const double* __restrict__ k44,
                                                 const int* __restrict__ fidx, int nv, const double* __restrict__ x,
                                                 double* __restrict__ y)
@@ -69,25 +71,33 @@ __global__ void __launch_bounds__(kCT) k_spmv44(const int* __restrict__ rowptr, 
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     if (r < n_nodes) {
         const int k1 = rowptr[r + 1];
-#pragma unroll 2
-        for (int k = rowptr[r] + lane; k < k1; k += L) {
-            const int c = __ldg(col + k);
-            const int fc = __ldg(fidx + c);
-            const double2* vp = reinterpret_cast<const double2*>(k44 + 16 * static_cast<int64_t>(k));
-            double2 v[8];
+        for (int k0 = rowptr[r] + lane; k0 < k1; k0 += PB * L) {
+            int2 c[PB];
+            double2 v[PB][8];
+            double xv[PB][4];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) v[q] = __ldg(vp + q);
-            double xv[4];
+            for (int p = 0; p < PB; ++p) {
+                const int k = k0 + p * L;
+                c[p] = k < k1 ? __ldg(cf + k) : make_int2(-1, -1);
+                const double2* vp = reinterpret_cast<const double2*>(k44 + 16 * static_cast<int64_t>(k < k1 ? k : k0));
 #pragma unroll
-            for (int j = 0; j < 3; ++j) xv[j] = fc >= 0 ? __ldg(x + 3 * static_cast<int64_t>(fc) + j) : 0.0;
-            xv[3] = __ldg(x + nv + c);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                acc[i] = fma(v[2 * i].x, xv[0], acc[i]);
-                acc[i] = fma(v[2 * i].y, xv[1], acc[i]);
-                acc[i] = fma(v[2 * i + 1].x, xv[2], acc[i]);
-                acc[i] = fma(v[2 * i + 1].y, xv[3], acc[i]);
+                for (int q = 0; q < 8; ++q) v[p][q] = __ldg(vp + q);
             }
+#pragma unroll
+            for (int p = 0; p < PB; ++p) {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) xv[p][j] = c[p].y >= 0 ? __ldg(x + 3 * static_cast<int64_t>(c[p].y) + j) : 0.0;
+                xv[p][3] = c[p].x >= 0 ? __ldg(x + nv + c[p].x) : 0.0;
+            }
+#pragma unroll
+            for (int p = 0; p < PB; ++p)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    acc[i] = fma(v[p][2 * i].x, xv[p][0], acc[i]);
+                    acc[i] = fma(v[p][2 * i].y, xv[p][1], acc[i]);
+                    acc[i] = fma(v[p][2 * i + 1].x, xv[p][2], acc[i]);
+                    acc[i] = fma(v[p][2 * i + 1].y, xv[p][3], acc[i]);
+                }
         }
     }
 #pragma unroll
@@ -118,10 +128,10 @@ void spmv44(const CoupledOp& K, const double* x, double* y, int nv, int np, cuda
 {
     if (K.n_nodes == 0) return;
     AcctScope acct(s, "k_spmv44", K.bytes(static_cast<int64_t>(nv) + np));
-    constexpr int L = 8;
+    constexpr int L = 8, PB = 2;
     const int64_t threads = static_cast<int64_t>(K.n_nodes) * L;
-    k_spmv44<L><<<static_cast<unsigned>((threads + kCT - 1) / kCT), kCT, 0, s>>>(K.rowptr, K.col, K.n_nodes, K.val.p,
-                                                                                 K.fidx, nv, x, y);
+    k_spmv44<L, PB><<<static_cast<unsigned>((threads + kCT - 1) / kCT), kCT, 0, s>>>(K.rowptr, K.cf, K.n_nodes,
+                                                                                     K.val.p, K.fidx, nv, x, y);
     after_launch("k_spmv44");
 }
 

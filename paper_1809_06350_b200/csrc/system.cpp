@@ -267,6 +267,12 @@ void ctx_build_mesh_system(Ctx& c)
     slot_dst(S.lB, srcB, c.dstB);
     slot_dst(S.lC, srcC, c.dstC);
     slot_dst(S.lD, srcD, c.dstD);
+    {
+        std::vector<int2> cf(PN.nnzb());
+        for (int64_t k = 0; k < PN.nnzb(); ++k) cf[k] = make_int2(PN.col[k], fidx[PN.col[k]]);
+        c.k44_cf.upload(cf, s);
+        ED_CUDA(cudaStreamSynchronize(s));
+    }
     c.sys_from_mesh = true;
     c.sys_values = false;
     ED_CUDA(cudaStreamSynchronize(s));
@@ -332,6 +338,7 @@ void make_work(Ctx& c, WorkSys& W, bool scale, double eps_diag)
         W.K.rowptr = S.D.st->rowptr.p;
         W.K.col = S.D.st->col.p;
         W.K.fidx = c.d_fidx.p;
+        W.K.cf = c.k44_cf.p;
         W.K.val.alloc(16 * static_cast<size_t>(W.K.nnzb));
     }
     if (!scale) {

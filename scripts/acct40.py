@@ -3,13 +3,13 @@ import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1809_06350_b200 import CubeProblem
 n = int(os.environ.get("N", "40"))
-cp = CubeProblem(n=n, nu=0.5)
+cp = CubeProblem(n=n, nu=0.5, dt=float(os.environ.get("DT", "1e-3")))
 ctx = cp.context(0)
 st = cp.seeded_state()
 ctx.set_state(st)
 ctx.state_save()
 opts = cp.solver_options()
-for _ in range(2):
+for _ in range(int(os.environ.get("WARM", "2"))):
     ctx.state_restore()
     out = ctx.newton_first_pass(cp.ts, opts)
 ctx.kernel_accounting(True)
