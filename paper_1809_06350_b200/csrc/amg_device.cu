@@ -868,7 +868,7 @@ DBsr upload_block(const HostCsr& a, int Rb, int Cb, cudaStream_t s)
 
 } // namespace
 
-Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s)
+Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s, LevelCache* cache)
 {
     Bsr out;
     if (!leveled) {
@@ -886,12 +886,39 @@ Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s)
         out.val = std::move(m.val);
         return out;
     }
-    return bsr_leveled(raw_of(m), s);
+    return bsr_leveled(raw_of(m), s, cache);
 }
 
-Bsr bsr_leveled(const DBsrRaw& m, cudaStream_t s)
+namespace {
+__global__ void k_same_pattern(const int* __restrict__ a, const int* __restrict__ b, int64_t n, int* diff)
+{
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n && a[i] != b[i]) *diff = 1;
+}
+} // namespace
+
+Bsr bsr_leveled(const DBsrRaw& m, cudaStream_t s, LevelCache* cache)
 {
     Bsr out;
+    const int E = m.Rb * m.Cb;
+    if (cache && cache->st && cache->nbr == m.nbr && cache->nbc == m.nbc && cache->nnzb == m.nnzb &&
+        cache->Rb == m.Rb && cache->Cb == m.Cb && std::getenv("ED_NO_LEVEL_CACHE") == nullptr) {
+        // same pattern as the previous build's level operator? (exact, on the device)
+        cache->flag.alloc(1);
+        cache->flag.zero(s);
+        k_same_pattern<<<g1(m.nbr + 1), kT, 0, s>>>(m.rowptr, cache->rowptr.p, m.nbr + 1, cache->flag.p);
+        if (m.nnzb) k_same_pattern<<<g1(m.nnzb), kT, 0, s>>>(m.col, cache->col.p, m.nnzb, cache->flag.p);
+        after_launch("k_same_pattern");
+        if (cache->flag.to_host(s)[0] == 0) {
+            out.st = cache->st;
+            out.val.alloc(std::max<int64_t>(m.nnzb * E, 1));
+            k_gather_rows<<<g1(m.nbr), kT, 0, s>>>(m.rowptr, m.val, out.st->perm.p ? out.st->perm.p : nullptr, m.nbr, E,
+                                                   out.st->rowptr.p, out.val.p);
+            after_launch("k_gather_rows");
+            ED_CUDA(cudaStreamSynchronize(s));
+            return out;
+        }
+    }
     // level schedule needs the pattern on the host
     const double t_start = now_ms_host();
     BlockPattern pat;
@@ -936,11 +963,22 @@ Bsr bsr_leveled(const DBsrRaw& m, cudaStream_t s)
                      "(%.1f ms host)\n",
                      m.nbr, static_cast<long long>(m.nnzb), out.st->nlev(), out.st->L, out.st->ring_cs, out.st->ngrp,
                      group_sweep_on(*out.st) ? "group sweep" : "legacy sweep", now_ms_host() - t_start);
-    const int E = m.Rb * m.Cb;
     out.val.alloc(std::max<int64_t>(m.nnzb * E, 1));
     k_gather_rows<<<g1(m.nbr), kT, 0, s>>>(m.rowptr, m.val, out.st->perm.p ? out.st->perm.p : nullptr, m.nbr, E,
                                            out.st->rowptr.p, out.val.p);
     after_launch("k_gather_rows");
+    if (cache) {
+        cache->nbr = m.nbr;
+        cache->nbc = m.nbc;
+        cache->nnzb = m.nnzb;
+        cache->Rb = m.Rb;
+        cache->Cb = m.Cb;
+        cache->rowptr.alloc(static_cast<size_t>(m.nbr) + 1);
+        ED_CUDA(cudaMemcpyAsync(cache->rowptr.p, m.rowptr, sizeof(int) * (m.nbr + 1), cudaMemcpyDeviceToDevice, s));
+        cache->col.alloc(std::max<int64_t>(m.nnzb, 1));
+        if (m.nnzb) ED_CUDA(cudaMemcpyAsync(cache->col.p, m.col, sizeof(int) * m.nnzb, cudaMemcpyDeviceToDevice, s));
+        cache->st = out.st;
+    }
     ED_CUDA(cudaStreamSynchronize(s));
     return out;
 }

@@ -76,8 +76,19 @@ void dense_vcycle_operator(const std::vector<DenseTailLevel>& lv, const std::vec
                            int pre_sweeps, int post_sweeps, DevArray<double>& out, cudaStream_t s);
 
 // Helpers shared with the V-cycle construction.
-Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s);
+// The structure of a level operator (level schedule, layout, sweep
+// structures) from the previous hierarchy build, with the pattern it was built
+// from: reused when the new level's pattern is exactly the same (checked on the
+// device), so only the values are gathered.
+struct LevelCache {
+    int nbr = -1, nbc = -1, Rb = 0, Cb = 0;
+    int64_t nnzb = -1;
+    DevArray<int> rowptr, col;
+    std::shared_ptr<BsrStruct> st;
+    DevArray<int> flag;
+};
+Bsr bsr_from_dbsr(DBsr&& m, bool leveled, cudaStream_t s, LevelCache* cache = nullptr);
 // the leveled (Gauss-Seidel level-ordered) operator of m; reads m only
-Bsr bsr_leveled(const DBsrRaw& m, cudaStream_t s);
+Bsr bsr_leveled(const DBsrRaw& m, cudaStream_t s, LevelCache* cache = nullptr);
 
 } // namespace edb

@@ -305,6 +305,7 @@ BsrLayout make_layout(const BlockPattern& pat, const std::vector<int>& row_order
         srp[s + 1] = srp[s] + (pat.rowptr[r + 1] - pat.rowptr[r]);
     }
     L.addr.assign(pat.nnzb(), -1);
+#pragma omp parallel for schedule(dynamic, 1024)
     for (int r = 0; r < n; ++r)
         for (int64_t k = pat.rowptr[r]; k < pat.rowptr[r + 1]; ++k) L.addr[k] = srp[L.inv[r]] + (k - pat.rowptr[r]);
     return L;
@@ -344,8 +345,12 @@ std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLay
     std::vector<int> dpos(n, -1);
     for (int s2 = 0; s2 < n; ++s2) {
         const int r = lay.perm[s2];
+        S.h_rowptr[s2 + 1] = static_cast<int>(S.h_rowptr[s2] + (pat.rowptr[r + 1] - pat.rowptr[r]));
+    }
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int s2 = 0; s2 < n; ++s2) {
+        const int r = lay.perm[s2];
         const int64_t len = pat.rowptr[r + 1] - pat.rowptr[r];
-        S.h_rowptr[s2 + 1] = static_cast<int>(S.h_rowptr[s2] + len);
         for (int64_t k = 0; k < len; ++k) {
             const int c = pat.col[pat.rowptr[r] + k];
             S.h_col[S.h_rowptr[s2] + k] = c;
@@ -448,16 +453,28 @@ void group_build(BsrStruct& S, cudaStream_t s)
     const bool identity = S.h_inv.empty();
     std::vector<unsigned char> code(S.nnzb, 0);
     std::vector<int> gptr(n + 1, 0), gblk;
+    std::vector<int> gcnt(n, 0);
+#pragma omp parallel for schedule(dynamic, 1024)
     for (int sr = 0; sr < n; ++sr) {
         const int row = identity ? sr : S.h_perm[sr];
+        int cnt = 0;
         for (int k = S.h_rowptr[sr]; k < S.h_rowptr[sr + 1]; ++k) {
             const int c = S.h_col[k];
             const int sc = identity ? c : S.h_inv[c];
             if (c == row) code[k] = 3;
             else if (grp_of[sr] >= 0 && grp_of[sc] == grp_of[sr]) code[k] = sc < sr ? 1 : 2;
-            if (grp_of[sr] >= 0 && code[k] != 0) gblk.push_back(k);
+            if (grp_of[sr] >= 0 && code[k] != 0) ++cnt;
         }
-        gptr[sr + 1] = static_cast<int>(gblk.size());
+        gcnt[sr] = cnt;
+    }
+    for (int sr = 0; sr < n; ++sr) gptr[sr + 1] = gptr[sr] + gcnt[sr];
+    gblk.resize(gptr[n]);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int sr = 0; sr < n; ++sr) {
+        if (grp_of[sr] < 0) continue;
+        int o = gptr[sr];
+        for (int k = S.h_rowptr[sr]; k < S.h_rowptr[sr + 1]; ++k)
+            if (code[k] != 0) gblk[o++] = k;
     }
     S.grp.upload(grp, s);
     S.grp_toff.upload(toff, s);

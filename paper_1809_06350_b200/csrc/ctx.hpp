@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include "amg_device.hpp"
 #include "amg_host.hpp"
 #include "assembly.hpp"
 #include "ed_internal.hpp"
@@ -181,6 +182,8 @@ struct Ctx {
     int csr_bv = -1;              // Bv the planes were last built with from csr_up
     // solver working set
     WorkSys work;
+    // level-operator structures of the previous hierarchy builds ([A, S_hat][level]), reused on identical patterns
+    LevelCache lcache[2][16];
     KrylovWs ws_outer, ws_a, ws_s;
     // timings of the last newton pass
     ed_phase_times times{};

@@ -196,17 +196,32 @@ __device__ __forceinline__ void grow_finish(const GrpArgs& a, double* z, double*
             for (int r = 0; r < B; ++r)
                 if (takes<FWD, MULTI>(P.code[q], r, d)) acc[r] = fma(P.v[q][r * B + d], zv[q][d], acc[r]);
     }
-    for (int k = P.kb + PF * L; k < P.ke; k += L) {
-        const int c = __ldg(a.col + k);
-        const int code = a.bcode[k];
-        const double* vp = a.val + static_cast<int64_t>(k) * (B * B);
+    // long rows (dense-row coarse levels: hundreds of blocks per lane): the
+    // rest in batches of NB blocks per lane, all of a batch's loads in flight
+    constexpr int NB = B == 3 ? 4 : 8;
+    for (int k0 = P.kb + PF * L; k0 < P.ke; k0 += NB * L) {
+        int cb[NB], codeb[NB];
+        double vb[NB][B * B], zb[NB][B];
 #pragma unroll
-        for (int d = 0; d < B; ++d) {
-            const double zz = __ldcg(z + static_cast<int64_t>(c) * B + d);
+        for (int p = 0; p < NB; ++p) {
+            const int k = k0 + p * L;
+            const bool in = k < P.ke;
+            cb[p] = in ? __ldg(a.col + k) : 0;
+            codeb[p] = in ? a.bcode[k] : -1;
 #pragma unroll
-            for (int r = 0; r < B; ++r)
-                if (takes<FWD, MULTI>(code, r, d)) acc[r] = fma(__ldg(vp + r * B + d), zz, acc[r]);
+            for (int e = 0; e < B * B; ++e) vb[p][e] = in ? __ldg(a.val + static_cast<int64_t>(k) * (B * B) + e) : 0.0;
         }
+#pragma unroll
+        for (int p = 0; p < NB; ++p)
+#pragma unroll
+            for (int d = 0; d < B; ++d) zb[p][d] = __ldcg(z + static_cast<int64_t>(cb[p]) * B + d);
+#pragma unroll
+        for (int p = 0; p < NB; ++p)
+#pragma unroll
+            for (int d = 0; d < B; ++d)
+#pragma unroll
+                for (int r = 0; r < B; ++r)
+                    if (codeb[p] >= 0 && takes<FWD, MULTI>(codeb[p], r, d)) acc[r] = fma(vb[p][r * B + d], zb[p][d], acc[r]);
     }
 #pragma unroll
     for (int r = 0; r < B; ++r) acc[r] = lane_sum<L>(acc[r]);

@@ -236,15 +236,32 @@ __device__ __forceinline__ void finish_row(const BsrArgs& m, double* z, bool val
 #pragma unroll
             for (int r = 0; r < B; ++r) acc[r] = use ? fma(P.v[q][r * B + d], zv[q][d], acc[r]) : acc[r];
     }
-    for (int k = P.kb + PF * L; k < P.ke; k += L) {
-        const int c = __ldg(m.col + k);
-        if (c == P.row) continue;
-        const double* vp = m.val + static_cast<int64_t>(k) * (B * B);
+    // long rows: the rest in batches of NB blocks per lane, all loads of a batch in flight
+    constexpr int NB = B == 3 ? 2 : 8;
+    for (int k0 = P.kb + PF * L; k0 < P.ke; k0 += NB * L) {
+        int cb[NB];
+        double vb[NB][B * B], zb[NB][B];
 #pragma unroll
-        for (int d = 0; d < B; ++d) {
-            const double zv = CG ? __ldcg(z + static_cast<int64_t>(c) * B + d) : z[static_cast<int64_t>(c) * B + d];
+        for (int p = 0; p < NB; ++p) {
+            const int k = k0 + p * L;
+            const bool in = k < P.ke;
+            cb[p] = in ? __ldg(m.col + k) : -1;
 #pragma unroll
-            for (int r = 0; r < B; ++r) acc[r] = fma(__ldg(vp + r * B + d), zv, acc[r]);
+            for (int e = 0; e < B * B; ++e) vb[p][e] = in ? __ldg(m.val + static_cast<int64_t>(k) * (B * B) + e) : 0.0;
+        }
+#pragma unroll
+        for (int p = 0; p < NB; ++p) {
+            const int64_t cc = cb[p] >= 0 ? cb[p] : 0;
+#pragma unroll
+            for (int d = 0; d < B; ++d) zb[p][d] = CG ? __ldcg(z + cc * B + d) : z[cc * B + d];
+        }
+#pragma unroll
+        for (int p = 0; p < NB; ++p) {
+            if (cb[p] < 0 || cb[p] == P.row) continue;
+#pragma unroll
+            for (int d = 0; d < B; ++d)
+#pragma unroll
+                for (int r = 0; r < B; ++r) acc[r] = fma(vb[p][r * B + d], zb[p][d], acc[r]);
         }
     }
 #pragma unroll
@@ -269,7 +286,7 @@ __device__ __forceinline__ void finish_row(const BsrArgs& m, double* z, bool val
 
 // One Gauss-Seidel half sweep over wide levels: persistent dataflow kernel.
 template <int B, int L, bool FWD>
-__global__ void __launch_bounds__(kThreads) k_sgs_flow(BsrArgs m, const double* __restrict__ bvec, double* z,
+__global__ void __launch_bounds__(kThreads, 2) k_sgs_flow(BsrArgs m, const double* __restrict__ bvec, double* z,
                                                        const double* __restrict__ invd, int nitems, int nlev,
                                                        const int* __restrict__ item_row,
                                                        const int* __restrict__ item_level,

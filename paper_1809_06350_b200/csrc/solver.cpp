@@ -250,6 +250,8 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
         };
         static const int tail_max = std::getenv("ED_DENSE_TAIL") ? std::atoi(std::getenv("ED_DENSE_TAIL")) : 4096;
         const bool tails = o.smoother == 1 && tail_max > 0;
+        // structure cache slot: the S_hat hierarchy is the one built on stream2
+        auto cache_of = [&](int l) -> LevelCache* { return l < 16 ? &c.lcache[s == c.stream2 ? 1 : 0][l] : nullptr; };
         cudaStream_t ts = s == c.stream ? c.stream3 : c.stream4;
         // The level-ordered operator of level 1 (host level schedule + ring
         // layout, the longest host step of the setup) is built on its own host
@@ -283,7 +285,7 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
                 try {
                     alloc_stream() = ts;
                     ED_CUDA(cudaSetDevice(c.device));
-                    pre_op = bsr_leveled(m, ts);
+                    pre_op = bsr_leveled(m, ts, cache_of(1));
                     ED_CUDA(cudaStreamSynchronize(ts));
                     host_lop = host_ms_acc();
                 } catch (...) {
@@ -359,7 +361,7 @@ void DevHierarchy::build(Ctx& c, const Bsr& A0, const AmgOpts& o, cudaStream_t s
                 d.Aown = std::move(pre_op);
                 d.A = &d.Aown;
             } else {
-                d.Aown = bsr_from_dbsr(std::move(D.A), true, s);
+                d.Aown = bsr_from_dbsr(std::move(D.A), true, s, cache_of(l));
                 d.A = &d.Aown;
             }
             d.invd = std::move(D.invd);
