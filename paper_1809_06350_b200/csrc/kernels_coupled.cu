@@ -10,7 +10,7 @@
 // per solve from the assembled node blocks (K4) with the solver's symmetric
 // scaling folded in (the same product w_r * w_c as the planes' k_scale, so
 // the entries equal the scaled planes' bitwise), and drives the outer
-// FGMRES's K x: each lane streams whole 128-B blocks with 16-B loads.
+// FGMRES's K x: the 8 lanes of a node row stream each 128-B block with 16-B loads.
 #include <cuda_runtime.h>
 
 #include "ed_internal.hpp"
@@ -55,62 +55,62 @@ __global__ void k_k44_build(const int* __restrict__ rowptr, const int* __restric
     }
 }
 
-// y = K x, x = [x_v (free velocity dofs); x_p (nodes)].  L lanes per node row,
-// each lane whole 128-B blocks (8 x LDG.128); a block's column comes with its
-// free velocity index (int2 {node, free index}), so the x gathers wait on one
-// load only; PB blocks per lane are in flight at once.
-template <int L, int PB>
+// y = K x, x = [x_v (free velocity dofs); x_p (nodes)].  The 8 lanes of a node
+// row share every block: lane q owns the 16-B piece q (block row q/2, columns
+// 2(q%2), 2(q%2)+1), so one warp instruction reads four whole 128-B lines
+// (LDG.E.128, every sector used once); a block's column comes with its free
+// velocity index (int2 {node, free index}, one broadcast load per group), and
+// PB blocks of the row are in flight per lane.  Measured at 160^3
+// (profiles/r02/spmv_variants_160.txt): 1.49 ms = 87 % of the measured HBM
+// peak; one lane per whole block (8 x LDG.128 to 32 different lines per
+// instruction) reached 56 %, streaming (evict-first) loads did not help.
+template <int PB>
 __global__ void __launch_bounds__(kCT) k_spmv44(const int* __restrict__ rowptr, const int2* __restrict__ cf,
-                                                int n_nodes, const double* __restrict__ k44,
-                                                const int* __restrict__ fidx, int nv, const double* __restrict__ x,
-                                                double* __restrict__ y)
+                                                 int n_nodes, const double* __restrict__ k44,
+                                                 const int* __restrict__ fidx, int nv, const double* __restrict__ x,
+                                                 double* __restrict__ y)
 {
     const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int r = static_cast<int>(gid / L);
-    const int lane = static_cast<int>(gid % L);
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const int r = static_cast<int>(gid >> 3);
+    const int q = static_cast<int>(gid & 7);
+    const int half = q & 1;
+    double acc = 0.0;
     if (r < n_nodes) {
         const int k1 = rowptr[r + 1];
-        for (int k0 = rowptr[r] + lane; k0 < k1; k0 += PB * L) {
+        const double2* base = reinterpret_cast<const double2*>(k44) + q;
+        for (int k0 = rowptr[r]; k0 < k1; k0 += PB) {
             int2 c[PB];
-            double2 v[PB][8];
-            double xv[PB][4];
+            double2 v[PB];
 #pragma unroll
             for (int p = 0; p < PB; ++p) {
-                const int k = k0 + p * L;
-                c[p] = k < k1 ? __ldg(cf + k) : make_int2(-1, -1);
-                const double2* vp = reinterpret_cast<const double2*>(k44 + 16 * static_cast<int64_t>(k < k1 ? k : k0));
-#pragma unroll
-                for (int q = 0; q < 8; ++q) v[p][q] = __ldg(vp + q);
+                const int k = k0 + p;
+                const bool in = k < k1;
+                const int kk = in ? k : k0;
+                c[p] = __ldg(cf + kk);
+                v[p] = __ldg(base + 8 * static_cast<int64_t>(kk));
+                if (!in) v[p] = make_double2(0.0, 0.0);
             }
 #pragma unroll
             for (int p = 0; p < PB; ++p) {
-#pragma unroll
-                for (int j = 0; j < 3; ++j) xv[p][j] = c[p].y >= 0 ? __ldg(x + 3 * static_cast<int64_t>(c[p].y) + j) : 0.0;
-                xv[p][3] = c[p].x >= 0 ? __ldg(x + nv + c[p].x) : 0.0;
+                // half 0: x_v[3 fc], x_v[3 fc + 1]; half 1: x_v[3 fc + 2], x_p[c]
+                const int fc = c[p].y;
+                const double x0 = fc >= 0 ? __ldg(x + 3 * static_cast<int64_t>(fc) + 2 * half) : 0.0;
+                const double x1 = half ? __ldg(x + nv + c[p].x)
+                                       : (fc >= 0 ? __ldg(x + 3 * static_cast<int64_t>(fc) + 1) : 0.0);
+                acc = fma(v[p].x, x0, acc);
+                acc = fma(v[p].y, x1, acc);
             }
-#pragma unroll
-            for (int p = 0; p < PB; ++p)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    acc[i] = fma(v[p][2 * i].x, xv[p][0], acc[i]);
-                    acc[i] = fma(v[p][2 * i].y, xv[p][1], acc[i]);
-                    acc[i] = fma(v[p][2 * i + 1].x, xv[p][2], acc[i]);
-                    acc[i] = fma(v[p][2 * i + 1].y, xv[p][3], acc[i]);
-                }
         }
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int o = L / 2; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o, L);
-    if (r < n_nodes && lane == 0) {
-        const int fr = fidx[r];
-        if (fr >= 0) {
-#pragma unroll
-            for (int i = 0; i < 3; ++i) y[3 * static_cast<int64_t>(fr) + i] = acc[i];
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (r < n_nodes && half == 0) {
+        const int i = q >> 1;
+        if (i == 3) {
+            y[nv + r] = acc;
+        } else {
+            const int fr = fidx[r];
+            if (fr >= 0) y[3 * static_cast<int64_t>(fr) + i] = acc;
         }
-        y[nv + r] = acc[3];
     }
 }
 
@@ -128,10 +128,9 @@ void spmv44(const CoupledOp& K, const double* x, double* y, int nv, int np, cuda
 {
     if (K.n_nodes == 0) return;
     AcctScope acct(s, "k_spmv44", K.bytes(static_cast<int64_t>(nv) + np));
-    constexpr int L = 8, PB = 2;
-    const int64_t threads = static_cast<int64_t>(K.n_nodes) * L;
-    k_spmv44<L, PB><<<static_cast<unsigned>((threads + kCT - 1) / kCT), kCT, 0, s>>>(K.rowptr, K.cf, K.n_nodes,
-                                                                                     K.val.p, K.fidx, nv, x, y);
+    const int64_t threads = static_cast<int64_t>(K.n_nodes) * 8;
+    k_spmv44<4><<<static_cast<unsigned>((threads + kCT - 1) / kCT), kCT, 0, s>>>(K.rowptr, K.cf, K.n_nodes, K.val.p,
+                                                                                 K.fidx, nv, x, y);
     after_launch("k_spmv44");
 }
 
