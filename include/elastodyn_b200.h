@@ -133,6 +133,28 @@ int ed_set_material(ed_ctx* ctx, const ed_material* mat);
 int ed_set_loads(ed_ctx* ctx, const double body_force[3], int n_facets,
                  const int32_t* facet_nodes, const double* facet_third, const double* facet_h);
 
+/* ---- cfg-3 enablers: extensions the reference does not have,
+ *      so their parity is pinned by this repo's own restatement only --------- */
+/* Per-element fibre structure tensors for material kind 1: h = [n_tets][2][9]
+ * (H_1, H_2 of each element, row-major), e.g. fibres in a local circumferential
+ * frame.  Replaces the global constants of the reference's DispersedFiberIsochoric
+ * (materials.cpp:67-80, materials.hpp:120-132); h == NULL returns to the
+ * material's global h1 / h2.  With every element's entry equal to the global
+ * tensors the assembly is bitwise the global-fibre one. */
+int ed_set_fiber_field(ed_ctx* ctx, int n_tets, const double* h);
+/* Prescribed displacement (inhomogeneous Dirichlet) for the NEXT
+ * ed_step_generalized_alpha call: u = [n][3] end-of-step displacement of the n
+ * listed nodes, which must be fully fixed (ED_INVALID_ARGUMENT otherwise).  The
+ * reference supports homogeneous constraints only (assembly.hpp:28-30): there
+ * the state at fixed nodes never changes.  Here, after the predictor
+ * (timeint.cpp:57-61), the iterate at those nodes is set to u and to the
+ * end-of-step rates the generalized-alpha update formulas give for it
+ * (udot = (u - u_n)/(gamma dt) + (gamma-1)/gamma udot_n, v = udot, vdot alike),
+ * so the stage blends (timeint.cpp:88-93) interpolate the boundary motion; the
+ * Newton increments stay zero there.  One-shot: consumed by the step.  n = 0
+ * clears a pending prescription. */
+int ed_set_prescribed_displacement(ed_ctx* ctx, int n, const int32_t* nodes, const double* u);
+
 /* ---- state (State, assembly.hpp:31-37): full-length host arrays ---------- */
 int ed_state_upload(ed_ctx* ctx, const double* u, const double* udot, const double* p,
                     const double* pdot, const double* v, const double* vdot);

@@ -38,12 +38,18 @@ def volumetric(mat, p):
     return rho, 1.0 / s, rho / s, -p / (s * s * s)
 
 
+def _hdot(H, M):
+    """ddot(H, M) per element for a global (3,3) or per-element (E,3,3) structure tensor."""
+    H = np.asarray(H)
+    return np.einsum("ij,eij->e", H, M) if H.ndim == 2 else np.einsum("eij,eij->e", H, M)
+
+
 def iso_stress(mat, Ct):
     """NeoHookeanIsochoric::stress (materials.hpp:108) / DispersedFiberIsochoric::stress (materials.cpp:32-41)."""
     S = np.zeros_like(Ct)
     S[:, 0, 0] = S[:, 1, 1] = S[:, 2, 2] = mat["mu"]
-    for H in mat.get("H", []):
-        E = np.einsum("ij,eij->e", H, Ct) - 1.0
+    for H in mat.get("H", []):  # H: (3,3) global (materials.cpp:67-80) or (E,3,3) per element (cfg-3 extension)
+        E = _hdot(H, Ct) - 1.0
         q = np.minimum(mat["k2"] * E * E, 500.0)
         S = S + (2.0 * mat["k1"] * E * np.exp(q))[:, None, None] * H
     return S
@@ -53,10 +59,10 @@ def iso_stress_dir(mat, Ct, dCt):
     """stress_dir (materials.hpp:109, materials.cpp:43-53)."""
     dS = np.zeros_like(Ct)
     for H in mat.get("H", []):
-        E = np.einsum("ij,eij->e", H, Ct) - 1.0
+        E = _hdot(H, Ct) - 1.0
         q = np.minimum(mat["k2"] * E * E, 500.0)
         c = 2.0 * mat["k1"] * (1.0 + 2.0 * mat["k2"] * E * E) * np.exp(q)
-        dS = dS + (c * np.einsum("ij,eij->e", H, dCt))[:, None, None] * H
+        dS = dS + (c * _hdot(H, dCt))[:, None, None] * H
     return dS
 
 
@@ -535,3 +541,87 @@ def solve_block_system(A, B, Cm, D, rhs, outer=(200, 200, 1e-6), ta=(500, 500, 1
         x = x * np.concatenate([wv, wp])
     stats.update(outer_iters=it, converged=int(conv))
     return x, stats, np.array(hist)
+
+
+# ---------------------------------------------------------------------------
+# timeint.cpp
+
+def step_generalized_alpha(mesh, dofs, mat, tau, loads, st, ts, solver, tol_R=1e-8, tol_A=1e-6, l_max=20,
+                           prescribed=None):
+    """step_generalized_alpha (timeint.cpp:40-180) on state dict `st` (updated copy returned with
+    the step statistics).  `solver` = keyword arguments of solve_block_system.
+
+    `prescribed` = (nodes, u_t) is the cfg-3 extension the reference lacks (homogeneous
+    constraints only, assembly.hpp:28-30): after the predictor the iterate at those fully fixed
+    nodes is set to the end-of-step displacement u_t [n,3] and to the rates the generalized-alpha
+    update formulas give for it: udot = (u_t - u_n)/(gamma dt) + (gamma-1)/gamma udot_n, v = udot,
+    vdot = (v - v_n)/(gamma dt) + (gamma-1)/gamma vdot_n."""
+    am, af, gam, dt = ts["alpha_m"], ts["alpha_f"], ts["gamma"], ts["dt"]
+    chi = af * gam * dt
+    gdt = gam * dt
+    nv, npn = dofs["nv"], dofs["np"]
+    flat = dofs["vdof"].reshape(-1)
+    idx = np.empty(nv, dtype=np.int64)
+    idx[flat[flat >= 0]] = np.nonzero(flat >= 0)[0]
+    keys = ("u", "udot", "p", "pdot", "v", "vdot")
+    yn = {k: np.array(st[k], dtype=np.float64) for k in keys}
+    cur = {k: yn[k].copy() for k in keys}
+    pf = (gam - 1.0) / gam
+    for k in ("udot", "pdot", "vdot"):
+        cur[k] = cur[k] * pf
+    if prescribed is not None:
+        nodes, u_t = prescribed
+        ii = (3 * np.asarray(nodes, dtype=np.int64)[:, None] + np.arange(3)[None, :]).reshape(-1)
+        ut = np.asarray(u_t, dtype=np.float64).reshape(-1)
+        cud = (ut - yn["u"][ii]) / gdt + pf * yn["udot"][ii]
+        cur["u"][ii] = ut
+        cur["udot"][ii] = cud
+        cur["v"][ii] = cud
+        cur["vdot"][ii] = (cud - yn["v"][ii]) / gdt + pf * yn["vdot"][ii]
+    blend = lambda a, b, w: a + w * (b - a)  # noqa: E731  (timeint.cpp:31-36)
+    out = dict(converged=False, newton_iters=0, res_history=[], linear=dict(
+        outer_iters=0, a_solves=0, a_iters=0, s_solves=0, s_iters=0, schur_applies=0, inner_iters=0))
+    norm_prev, prev = np.inf, None
+    for l in range(1, l_max + 2):
+        halvings = 0
+        while True:
+            mid = {k: blend(yn[k], cur[k], am if k in ("udot", "pdot", "vdot") else af) for k in keys}
+            admissible = True
+            try:
+                rm, rp = assemble_residuals(mesh, dofs, mat, tau, loads, mid)
+            except RuntimeError:
+                admissible = False
+            if admissible:
+                rk = mid["udot"][idx] - mid["v"][idx]
+                norm = math.sqrt(rk @ rk + rp @ rp + rm @ rm)
+                if np.isfinite(norm) and norm <= 4.0 * norm_prev:
+                    break
+            if l == 1 or halvings >= 30:
+                return cur, out
+            cur = {k: blend(prev[k], cur[k], 0.5) for k in keys}
+            halvings += 1
+        out["res_history"].append(norm)
+        norm_prev = norm
+        if l == 1:
+            res0 = norm
+        if norm <= max(tol_R * res0, tol_A):
+            out["converged"] = True
+            return cur, out
+        if l > l_max:
+            break
+        A, B, Cm, D, Ar, Cr = assemble_tangent(mesh, dofs, mat, tau, loads, mid, ts)
+        rhs = np.concatenate([-rm + (A @ rk - Ar @ rk) / chi, -rp + (Cm @ rk - Cr @ rk) / chi])
+        x, stats, _ = solve_block_system(A, B, Cm, D, rhs, **solver)
+        for k in out["linear"]:
+            out["linear"][k] += stats[k]
+        out["newton_iters"] += 1
+        prev = {k: cur[k].copy() for k in keys}
+        dvd = x[:nv]
+        dud = (chi / am) * dvd - rk / am
+        cur["vdot"][idx] += dvd
+        cur["v"][idx] += gdt * dvd
+        cur["udot"][idx] += dud
+        cur["u"][idx] += gdt * dud
+        cur["pdot"] += x[nv:]
+        cur["p"] += gdt * x[nv:]
+    return cur, out

@@ -117,6 +117,13 @@ def dispersed_fiber(mu, k1, k2, kd, phi_deg, rho0, kappa=None) -> N.Material:
     return m
 
 
+def fiber_structure_tensors(dirs, kd) -> np.ndarray:
+    """H = kd I + (1 - 3 kd) a (x) a (materials.cpp:8-19) for an array of unit
+    directions dirs[..., 3] -> [..., 3, 3]."""
+    dirs = np.asarray(dirs, dtype=np.float64)
+    return np.eye(3) * kd + (1.0 - 3.0 * kd) * dirs[..., :, None] * dirs[..., None, :]
+
+
 def wave_speed(mat: N.Material) -> float:
     """Material::wave_speed (materials.hpp:148-152)."""
     if mat.incompressible:
@@ -232,6 +239,25 @@ class Context:
             return
         fn, th, fh = N.i32(np.asarray(facet_nodes).reshape(-1)), N.f64(facet_third), N.f64(np.asarray(facet_h).reshape(-1))
         self._chk(N.lib().ed_set_loads(self._p, N.dp(bf), len(th), N.ip(fn), N.dp(th), N.dp(fh)))
+
+    def set_fiber_field(self, h):
+        """Per-element fibre structure tensors [E, 2, 3, 3] (None: the material's global ones).
+        Extension of materials.cpp:67-80 (global fibre constants) for local fibre frames."""
+        if h is None:
+            self._chk(N.lib().ed_set_fiber_field(self._p, 0, None))
+            return
+        hh = N.f64(np.asarray(h).reshape(-1))
+        self._chk(N.lib().ed_set_fiber_field(self._p, hh.size // 18, N.dp(hh)))
+
+    def set_prescribed_displacement(self, nodes, u):
+        """End-of-step displacement [n, 3] of fully fixed nodes for the next step() call
+        (inhomogeneous Dirichlet; the reference has homogeneous constraints only, assembly.hpp:28-30)."""
+        nn = N.i32(np.asarray(nodes).reshape(-1))
+        uu = N.f64(np.asarray(u).reshape(-1))
+        if uu.size != 3 * nn.size:
+            raise ValueError("prescribed displacement: 3 values per node")
+        self._chk(N.lib().ed_set_prescribed_displacement(self._p, nn.size, N.ip(nn) if nn.size else None,
+                                                         N.dp(uu) if nn.size else None))
 
     def set_state(self, s: State):
         arrs = s.arrays()

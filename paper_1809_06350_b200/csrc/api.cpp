@@ -317,6 +317,7 @@ AsmArgs asm_args(Ctx& c, bool stage)
     A.fp = c.fp.p;
     A.bad_element = c.dscratch_i.p;
     A.mat = c.mat;
+    A.elem_h = c.elem_h.n ? c.elem_h.p : nullptr;
     for (int i = 0; i < 3; ++i) A.body_force[i] = c.body_force[i];
     return A;
 }
@@ -492,6 +493,8 @@ int ed_mesh_upload(ed_ctx* ctx, int n_nodes, int n_tets, const int32_t* tets, co
         c.have_mesh = true;
         c.have_dofs = false;
         c.sys_from_mesh = false;
+        c.elem_h = DevArray<double>();
+        c.pd_n = 0;
     });
 }
 
@@ -548,6 +551,38 @@ int ed_set_material(ed_ctx* ctx, const ed_material* mat)
         check(mat->incompressible || mat->kappa > 0.0, ED_INVALID_ARGUMENT, "kappa must be positive");
         c.mat = *mat;
         c.have_mat = true;
+    });
+}
+
+int ed_set_fiber_field(ed_ctx* ctx, int n_tets, const double* h)
+{
+    return guarded(ctx, [&](Ctx& c) {
+        check(c.have_mesh, ED_NOT_READY, "mesh required");
+        if (h == nullptr) { // back to the material's global structure tensors
+            c.elem_h = DevArray<double>();
+            return;
+        }
+        check(n_tets == c.n_tets, ED_INVALID_ARGUMENT, "fibre field: one entry per element");
+        c.elem_h.upload(h, 18LL * n_tets, c.stream);
+        c.sync();
+    });
+}
+
+int ed_set_prescribed_displacement(ed_ctx* ctx, int n, const int32_t* nodes, const double* u)
+{
+    return guarded(ctx, [&](Ctx& c) {
+        check(c.have_dofs, ED_NOT_READY, "dofs required");
+        c.pd_n = 0;
+        if (n == 0) return;
+        check(n > 0 && nodes && u, ED_INVALID_ARGUMENT, "bad prescribed-displacement arguments");
+        for (int i = 0; i < n; ++i) {
+            check(nodes[i] >= 0 && nodes[i] < c.n_nodes, ED_INVALID_ARGUMENT, "prescribed node out of range");
+            check(c.fidx[nodes[i]] < 0, ED_INVALID_ARGUMENT, "prescribed displacement on a free node");
+        }
+        c.pd_nodes.upload(nodes, n, c.stream);
+        c.pd_u.upload(u, 3LL * n, c.stream);
+        c.sync();
+        c.pd_n = n;
     });
 }
 
@@ -870,6 +905,11 @@ int ed_step_generalized_alpha(ed_ctx* ctx, const ed_time_scalars* ts, const ed_n
         nh.yn_vdot = c.q_vdot.p;
         // predictor + first stage blend (timeint.cpp:57-61, 88-93)
         launch_predict_blend(na, s);
+        if (c.pd_n > 0) { // prescribed boundary motion of this step (one-shot)
+            launch_prescribe(c.pd_nodes.p, c.pd_u.p, c.pd_n, na, gdt, s);
+            launch_stage_blend(na, s);
+            c.pd_n = 0;
+        }
         ed_step_stats st{};
         Stats lin;
         std::vector<double> hist;

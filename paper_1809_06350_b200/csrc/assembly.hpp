@@ -11,6 +11,7 @@ struct AsmArgs {
     const double* volume = nullptr;
     const double* tau = nullptr;
     const int* fidx = nullptr; // node -> free index or -1
+    const double* elem_h = nullptr; // [E][2][9] per-element fibre structure tensors, or null (global)
     const double *u = nullptr, *udot = nullptr, *p = nullptr, *pdot = nullptr, *v = nullptr, *vdot = nullptr;
     const double* rk = nullptr; // kinematic residual (nv) for the fold-in, or null
     const int* elem_order = nullptr;
@@ -82,6 +83,11 @@ struct NewtonArgs {
     double pf, alpha_m, alpha_f;
 };
 void launch_predict_blend(const NewtonArgs& a, cudaStream_t s);
+// Prescribed boundary motion (extension; the reference has homogeneous constraints only,
+// assembly.hpp:28-30): at the listed fully fixed nodes cur_u = u_t and the end-of-step
+// rates follow the generalized-alpha update formulas, cur_udot = (u_t - u_n)/(gamma dt) + pf udot_n,
+// cur_v = cur_udot, cur_vdot = (cur_v - v_n)/(gamma dt) + pf vdot_n.
+void launch_prescribe(const int* nodes, const double* u_t, int n, const NewtonArgs& a, double gdt, cudaStream_t s);
 // mid = blend(yn, cur) (timeint.cpp:88-93)
 void launch_stage_blend(const NewtonArgs& a, cudaStream_t s);
 // cur = blend(prev, cur, 0.5) with prev in the yn_* slots (timeint.cpp:131-136)

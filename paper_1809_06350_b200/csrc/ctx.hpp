@@ -160,6 +160,11 @@ struct Ctx {
     DevArray<int> dstA, dstB, dstC, dstD; // inverse maps: stored block of each K4 slot per plane (-1: none)
     DevArray<int2> k44_cf;                // per node-graph block {column node, its free index} (coupled SpMV)
     ed_material mat{};
+    DevArray<double> elem_h; // [E][2][9] per-element fibre structure tensors (empty: the material's global ones)
+    // prescribed end-of-step displacement of fully fixed nodes, consumed by the next time step
+    DevArray<int> pd_nodes;
+    DevArray<double> pd_u;
+    int pd_n = 0;
     double body_force[3] = {0.0, 0.0, 0.0};
     DevArray<int64_t> tr_rowptr;
     DevArray<int> tr_rows;

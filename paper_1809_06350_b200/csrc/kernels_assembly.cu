@@ -132,12 +132,13 @@ __device__ __forceinline__ Vol volumetric(const ed_material& m, double p)
     return v;
 }
 
-__device__ __forceinline__ void iso_stress(const ed_material& m, const double* Ct, double* S)
+// Hs: the element's two fibre structure tensors (the material's global ones,
+// materials.cpp:67-80, or the element's entry of the fibre field)
+__device__ __forceinline__ void iso_stress(const ed_material& m, const double (*Hs)[9], const double* Ct, double* S)
 {
 #pragma unroll
     for (int k = 0; k < 9; ++k) S[k] = (k == 0 || k == 4 || k == 8) ? m.mu : 0.0;
     if (m.kind == 1) {
-        const double* Hs[2] = {m.h1, m.h2};
 #pragma unroll
         for (int f = 0; f < 2; ++f) {
             const double* H = Hs[f];
@@ -150,13 +151,12 @@ __device__ __forceinline__ void iso_stress(const ed_material& m, const double* C
     }
 }
 
-__device__ __forceinline__ void iso_stress_dir(const ed_material& m, const double* Ct, const double* dCt,
-                                               double* dS)
+__device__ __forceinline__ void iso_stress_dir(const ed_material& m, const double (*Hs)[9], const double* Ct,
+                                               const double* dCt, double* dS)
 {
 #pragma unroll
     for (int k = 0; k < 9; ++k) dS[k] = 0.0;
     if (m.kind == 1) {
-        const double* Hs[2] = {m.h1, m.h2};
 #pragma unroll
         for (int f = 0; f < 2; ++f) {
             const double* H = Hs[f];
@@ -183,6 +183,7 @@ struct Frame {
     // per quadrature point
     double pq[4], pdq[4], vdq[4][3], rho[4], beta[4], drho[4], dbeta[4], vmb[4][3], res[4][3], cont[4];
     double dP[12][9];
+    double H[2][9]; // fibre structure tensors of this element (kind 1)
     int nodes[4];
     int free_idx[4];
     int valid;
@@ -214,7 +215,7 @@ __device__ void ptilde_dir(const ed_material& m, const Frame& f, int bn, int j, 
 #pragma unroll
     for (int k = 0; k < 9; ++k) dCt[k] = dC[k] * f.Jm23 + dJm23 * f.C[k];
     double dS[9];
-    iso_stress_dir(m, f.Ct, dCt, dS);
+    iso_stress_dir(m, f.H, f.Ct, dCt, dS);
     double tmp[9], dCinv[9];
     matmul3(dC, f.Cinv, tmp);
     matmul3(f.Cinv, tmp, dCinv);
@@ -268,6 +269,13 @@ __device__ void build_frame(const AsmArgs& A, Frame& f, int e, int lane, bool ac
         f.vol = A.volume[e];
         f.tau = A.tau[e];
     }
+    if (active && A.mat.kind == 1 && (lane == 5 || lane == 6)) {
+        // per-element fibre field (local frames) or the material's global tensors
+        const int fam = lane - 5;
+        const double* H = A.elem_h ? A.elem_h + 18 * static_cast<int64_t>(e) + 9 * fam : (fam ? A.mat.h2 : A.mat.h1);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) f.H[fam][k] = H[k];
+    }
     __syncthreads();
     // --- B: kinematics + stress (Kinematics::from_F, evaluate_stress).  The
     // three independent chains -- F^-1; C = F^T F and C^-1; J^-2/3 -- run on
@@ -303,7 +311,7 @@ __device__ void build_frame(const AsmArgs& A, Frame& f, int e, int lane, bool ac
     if (f.valid && lane == 0) {
 #pragma unroll
         for (int k = 0; k < 9; ++k) f.Ct[k] = f.C[k] * f.Jm23;
-        iso_stress(A.mat, f.Ct, f.St);
+        iso_stress(A.mat, f.H, f.Ct, f.St);
         const double sc = ddot3(f.St, f.Ct);
         const double c1 = -sc / 3.0;
 #pragma unroll

@@ -142,6 +142,20 @@ __global__ void k_predict_blend(NewtonArgs a)
     }
 }
 
+__global__ void k_prescribe(const int* __restrict__ nodes, const double* __restrict__ u_t, int n, NewtonArgs a,
+                            double gdt)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * n) return;
+    const int64_t idx = 3 * static_cast<int64_t>(nodes[i / 3]) + i % 3;
+    const double ut = u_t[i];
+    const double cud = (ut - a.yn_u[idx]) / gdt + a.pf * a.yn_udot[idx];
+    a.cur_u[idx] = ut;
+    a.cur_udot[idx] = cud;
+    a.cur_v[idx] = cud;
+    a.cur_vdot[idx] = (cud - a.yn_v[idx]) / gdt + a.pf * a.yn_vdot[idx];
+}
+
 // stage blends only (timeint.cpp:88-93): mid = blend(yn, cur)
 __global__ void k_stage_blend(NewtonArgs a)
 {
@@ -258,6 +272,13 @@ void launch_predict_blend(const NewtonArgs& a, cudaStream_t s)
 {
     k_predict_blend<<<g1(3 * static_cast<int64_t>(a.n_nodes)), 256, 0, s>>>(a);
     after_launch("k_predict_blend");
+}
+
+void launch_prescribe(const int* nodes, const double* u_t, int n, const NewtonArgs& a, double gdt, cudaStream_t s)
+{
+    if (n == 0) return;
+    k_prescribe<<<g1(3 * static_cast<int64_t>(n)), 256, 0, s>>>(nodes, u_t, n, a, gdt);
+    after_launch("k_prescribe");
 }
 
 void launch_stage_blend(const NewtonArgs& a, cudaStream_t s)

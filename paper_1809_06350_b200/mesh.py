@@ -107,8 +107,29 @@ def generate_box_mesh(nx, ny, nz, lx, ly, lz) -> Mesh:
     for b in range(8):
         corner[:, b] = (ci + (b & 1)) + mx * ((cj + ((b >> 1) & 1)) + my * (ck + ((b >> 2) & 1)))
     tets = corner[:, CELL_TETS].reshape(-1, 4)
+    tets, volume, grad, h = _finalize_geometry(nodes, tets)
 
-    # finalize_geometry (mesh.cpp:77-123)
+    # collect_boundary_facets (mesh.cpp:125-154)
+    tol = 1e-12 * max(lx, ly, lz, 1.0)
+    lims = (lx, ly, lz)
+    tri = tets[:, FACE]  # (E, 4, 3)
+    pts = nodes[tri]     # (E, 4, 3, 3)
+    plane = np.full(tri.shape[:2], -1, dtype=np.int64)
+    for d in range(2, -1, -1):  # first matching d wins in the reference -> iterate reversed
+        lo = np.all(np.abs(pts[..., d]) < tol, axis=-1)
+        hi = np.all(np.abs(pts[..., d] - lims[d]) < tol, axis=-1)
+        plane = np.where(hi, 2 * d + 1, plane)
+        plane = np.where(lo, 2 * d, plane)
+    e_idx, f_idx = np.nonzero(plane >= 0)
+    order = np.lexsort((f_idx, e_idx))
+    e_idx, f_idx = e_idx[order], f_idx[order]
+    return Mesh(nodes=nodes, tets=tets.astype(np.int32), volume=volume, h=h, grad_n=grad,
+                facet_nodes=tri[e_idx, f_idx].astype(np.int32), facet_tet=e_idx.astype(np.int32),
+                facet_tag=plane[e_idx, f_idx].astype(np.int32), tag_names=list(TAGS))
+
+
+def _finalize_geometry(nodes, tets):
+    """finalize_geometry (mesh.cpp:77-123): orientation, volume, shape-function gradients, h."""
     def edge_mat(t):
         x0 = nodes[t[:, 0]]
         dm = np.empty((t.shape[0], 9))
@@ -140,25 +161,65 @@ def generate_box_mesh(nx, ny, nz, lx, ly, lz) -> Mesh:
         for b in range(a + 1, 4):
             h = np.maximum(h, _norm(nodes[tets[:, a]] - nodes[tets[:, b]]))
 
-    # collect_boundary_facets (mesh.cpp:125-154)
-    tol = 1e-12 * max(lx, ly, lz, 1.0)
-    lims = (lx, ly, lz)
-    tri = tets[:, FACE]  # (E, 4, 3)
-    pts = nodes[tri]     # (E, 4, 3, 3)
-    plane = np.full(tri.shape[:2], -1, dtype=np.int64)
-    for d in range(2, -1, -1):  # first matching d wins in the reference -> iterate reversed
-        lo = np.all(np.abs(pts[..., d]) < tol, axis=-1)
-        hi = np.all(np.abs(pts[..., d] - lims[d]) < tol, axis=-1)
-        plane = np.where(hi, 2 * d + 1, plane)
-        plane = np.where(lo, 2 * d, plane)
-    e_idx, f_idx = np.nonzero(plane >= 0)
-    order = np.lexsort((f_idx, e_idx))
-    e_idx, f_idx = e_idx[order], f_idx[order]
-    return Mesh(nodes=nodes, tets=tets.astype(np.int32), volume=volume, h=h, grad_n=grad,
-                facet_nodes=tri[e_idx, f_idx].astype(np.int32), facet_tet=e_idx.astype(np.int32),
-                facet_tag=plane[e_idx, f_idx].astype(np.int32), tag_names=list(TAGS))
+    return tets, volume, grad, h
 
 
 def generate_cube_mesh(n, edge_length) -> Mesh:
     """generate_cube_mesh (mesh.cpp:190-193)."""
     return generate_box_mesh(n, n, n, edge_length, edge_length, edge_length)
+
+
+CYL_TAGS = ("rmin", "rmax", "zmin", "zmax")
+
+
+def generate_cylinder_mesh(n_r, n_theta, n_z, r_in, thickness, length) -> Mesh:
+    """Thick-walled cylinder about the z axis (BASELINE configs[3]; the reference
+    has boxes only, mesh.hpp:52-60): n_r x n_theta x n_z hexes in (r, theta, z),
+    periodic in theta, each split into six tets on its 0-7 diagonal exactly like
+    the box generator (cell corner bit 0 = r, bit 1 = theta, bit 2 = z), then
+    the reference's finalize_geometry.  Nodes are numbered
+    ``i_r + (n_r + 1) (j_theta + n_theta k_z)``.  Boundary facets are tagged
+    rmin / rmax / zmin / zmax."""
+    if min(n_r, n_z) < 1 or n_theta < 3:
+        raise ValueError("divisions must be >= 1 (>= 3 around the circumference)")
+    if r_in <= 0.0 or thickness <= 0.0 or length <= 0.0:
+        raise ValueError("radii and length must be positive")
+    mr, mz = n_r + 1, n_z + 1
+    k, j, i = np.meshgrid(np.arange(mz), np.arange(n_theta), np.arange(mr), indexing="ij")
+    r = r_in + thickness * i.ravel() / n_r
+    th = 2.0 * np.pi * j.ravel() / n_theta
+    nodes = np.stack([r * np.cos(th), r * np.sin(th), length * k.ravel() / n_z], axis=1)
+    ck, cj, ci = np.meshgrid(np.arange(n_z), np.arange(n_theta), np.arange(n_r), indexing="ij")
+    ci, cj, ck = ci.ravel(), cj.ravel(), ck.ravel()
+    corner = np.empty((ci.size, 8), dtype=np.int64)
+    for b in range(8):
+        corner[:, b] = (ci + (b & 1)) + mr * (((cj + ((b >> 1) & 1)) % n_theta) + n_theta * (ck + ((b >> 2) & 1)))
+    tets = corner[:, CELL_TETS].reshape(-1, 4)
+    tets, volume, grad, h = _finalize_geometry(nodes, tets)
+    # boundary facets from the logical coordinates of the facet's nodes
+    tri = tets[:, FACE]
+    ir = tri % mr
+    kz = tri // (mr * n_theta)
+    plane = np.full(tri.shape[:2], -1, dtype=np.int64)
+    plane = np.where(np.all(kz == n_z, axis=-1), 3, plane)
+    plane = np.where(np.all(kz == 0, axis=-1), 2, plane)
+    plane = np.where(np.all(ir == n_r, axis=-1), 1, plane)
+    plane = np.where(np.all(ir == 0, axis=-1), 0, plane)
+    e_idx, f_idx = np.nonzero(plane >= 0)
+    order = np.lexsort((f_idx, e_idx))
+    e_idx, f_idx = e_idx[order], f_idx[order]
+    return Mesh(nodes=nodes, tets=tets.astype(np.int32), volume=volume, h=h, grad_n=grad,
+                facet_nodes=tri[e_idx, f_idx].astype(np.int32), facet_tet=e_idx.astype(np.int32),
+                facet_tag=plane[e_idx, f_idx].astype(np.int32), tag_names=list(CYL_TAGS))
+
+
+def circumferential_fiber_dirs(mesh: Mesh, phi_deg: float) -> np.ndarray:
+    """Two fibre families per element at +-phi to the circumferential direction in the
+    (theta, z) tangent plane of a cylinder about the z axis, evaluated at the element
+    centroid: a = cos(phi) e_theta +- sin(phi) e_z.  Returns [E, 2, 3] unit vectors."""
+    c = mesh.nodes[mesh.tets].mean(axis=1)
+    rr = np.sqrt(c[:, 0] * c[:, 0] + c[:, 1] * c[:, 1])
+    e_t = np.stack([-c[:, 1] / rr, c[:, 0] / rr, np.zeros_like(rr)], axis=1)
+    e_z = np.array([0.0, 0.0, 1.0])
+    phi = phi_deg * np.pi / 180.0
+    return np.stack([np.cos(phi) * e_t + np.sin(phi) * e_z, np.cos(phi) * e_t - np.sin(phi) * e_z], axis=1)

@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import api
-from .mesh import Mesh, generate_cube_mesh
+from .mesh import Mesh, circumferential_fiber_dirs, generate_cube_mesh, generate_cylinder_mesh
 
 CONFIGS = {
     0: dict(n=10, nu=0.4, steps=5, seeded=False),
@@ -122,4 +122,77 @@ class CubeProblem:
         ctx.build_dofs(self.fixed)
         ctx.set_material(self.material)
         ctx.set_loads((0.0, 0.0, 0.0), self.load_facets, self.load_third, self.traction_h())
+        return ctx
+
+
+@dataclass
+class CylinderProblem:
+    """BASELINE configs[3]: tensile test of an anisotropic arterial wall.
+
+    Thick-walled cylinder (inner radius 1 cm, wall 0.1 cm, length 1 cm, SI units),
+    n_r x n_theta x n_z hexes split into six tets; fully incompressible
+    Neo-Hookean ground matrix mu with two fibre families at +-phi to the
+    circumferential direction in the local tangent plane (per-element structure
+    tensors H = kd I + (1 - 3 kd) a (x) a, the reference's DispersedFiberIsochoric
+    energy, materials.cpp:21-53, evaluated with the element's own a); the z = 0
+    end is clamped, the z = L end carries a prescribed axial displacement ramped
+    linearly to `stretch` L over `n_steps` generalized-alpha steps.
+
+    The reference cannot run this configuration (boxes only, global fibres,
+    homogeneous constraints), so it is pinned by oracle/restate.py alone.
+    Choices BASELINE leaves open: kd = 0 (no dispersion), no fibre tension switch
+    (as in the reference's energy), both ends fully clamped in all three
+    components (nodes here are fully free or fully fixed), dt = 1e-3.
+    """
+    n_r: int = 8
+    n_theta: int = 128
+    n_z: int = 64
+    r_in: float = 1.0e-2
+    thickness: float = 1.0e-3
+    length: float = 1.0e-2
+    mu: float = 3.0e4
+    k1: float = 2.3632e5
+    k2: float = 0.8393
+    kd: float = 0.0
+    phi_deg: float = 49.98
+    rho0: float = 1.0e3
+    c_m: float = 1e-3
+    stretch: float = 0.10
+    n_steps: int = 10
+    dt: float = 1e-3
+    rho_inf: float = 0.5
+
+    def __post_init__(self):
+        self.mesh: Mesh = generate_cylinder_mesh(self.n_r, self.n_theta, self.n_z, self.r_in, self.thickness,
+                                                 self.length)
+        kz = np.arange(self.mesh.n_nodes) // ((self.n_r + 1) * self.n_theta)
+        self.bottom_nodes = np.nonzero(kz == 0)[0].astype(np.int32)
+        self.top_nodes = np.nonzero(kz == self.n_z)[0].astype(np.int32)
+        self.fixed = np.zeros((self.mesh.n_nodes, 3), dtype=bool)
+        self.fixed[self.bottom_nodes] = True
+        self.fixed[self.top_nodes] = True
+        self.material = api.dispersed_fiber(self.mu, self.k1, self.k2, self.kd, self.phi_deg, self.rho0)
+        self.fiber_dirs = circumferential_fiber_dirs(self.mesh, self.phi_deg)           # [E, 2, 3]
+        self.fiber_field = api.fiber_structure_tensors(self.fiber_dirs, self.kd)        # [E, 2, 3, 3]
+        self.tau = api.compute_tau(self.mesh, self.material, self.c_m)
+        self.ts = api.gen_alpha_scalars(self.rho_inf, self.dt)
+        self.n_free = int((~self.fixed[:, 0]).sum())
+        self.nv = 3 * self.n_free
+        self.np = self.mesh.n_nodes
+
+    def top_displacement(self, step: int) -> np.ndarray:
+        """Prescribed displacement [n_top, 3] at the end of time step `step` (1-based), linear ramp."""
+        u = np.zeros((len(self.top_nodes), 3))
+        u[:, 2] = self.stretch * self.length * min(step, self.n_steps) / self.n_steps
+        return u
+
+    solver_options = CubeProblem.solver_options
+
+    def context(self, device: int = 0) -> api.Context:
+        ctx = api.Context(device)
+        ctx.set_mesh(self.mesh, self.tau)
+        ctx.build_dofs(self.fixed)
+        ctx.set_material(self.material)
+        ctx.set_fiber_field(self.fiber_field)
+        ctx.set_loads((0.0, 0.0, 0.0))
         return ctx

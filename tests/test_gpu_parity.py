@@ -542,3 +542,157 @@ def test_reference_side_cpp_binding_runs():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, (r.stdout, r.stderr)
+
+
+# --------------------------------------------------------------------------
+# cfg-3 enablers.  The reference has none of them (boxes only,
+# global fibres, homogeneous constraints), so the oracle here is the numpy
+# restatement, extended the same way and pinned to the reference on everything
+# the extension leaves unchanged (tests/test_oracle_cpu.py: restated time step,
+# uniform fibre field == global fibres).
+
+def _restate_cylinder(cy):
+    m = cy.mesh
+    vdof = np.full((m.n_nodes, 3), -1, dtype=np.int64)
+    free = ~cy.fixed[:, 0]
+    vdof[free] = np.arange(3 * int(free.sum())).reshape(-1, 3)
+    mesh = dict(tets=m.tets.astype(np.int64), grad_n=m.grad_n, volume=m.volume)
+    dofs = dict(vdof=vdof, nv=cy.nv, np=cy.np)
+    mat = dict(incompressible=True, rho0=cy.rho0, mu=cy.mu, kappa=0.0, k1=cy.k1, k2=cy.k2,
+               H=[cy.fiber_field[:, 0], cy.fiber_field[:, 1]])
+    loads = dict(body_force=(0.0, 0.0, 0.0), facets=[])
+    ts = dict(dt=cy.dt, alpha_m=cy.ts.alpha_m, alpha_f=cy.ts.alpha_f, gamma=cy.ts.gamma)
+    return mesh, dofs, mat, loads, ts
+
+
+def _strained_cylinder_state(cy, seed=7):
+    """A smooth 5 % axial stretch plus seeded noise, so the fibres are engaged."""
+    from paper_1809_06350_b200.problem import splitmix64, uniform
+    N = cy.mesh.n_nodes
+    bits = splitmix64(seed, 7 * N)
+    st = api.State.zeros(N)
+    u = np.zeros((N, 3))
+    u[:, 2] = 0.05 * cy.mesh.nodes[:, 2]
+    st.u = (u + 1e-5 * uniform(bits[: 3 * N], -1.0, 1.0).reshape(N, 3)).reshape(-1)
+    st.v = uniform(bits[3 * N: 6 * N], -1e-3, 1e-3)
+    st.p = uniform(bits[6 * N: 7 * N], -1e2, 1e2)
+    return st
+
+
+def test_uniform_fiber_field_is_bitwise_the_global_fibers():
+    """ed_set_fiber_field with every element's entry equal to the material's global structure
+    tensors (materials.cpp:67-80) reproduces the reference-pinned global-fibre assembly bit for bit."""
+    cp = CubeProblem(n=4, nu=0.5)
+    mat = api.dispersed_fiber(2.0, 1.5, 0.8, 0.1, 40.0, 1.0)
+    st = cp.seeded_state()
+    st.u *= 20.0
+    outs = []
+    for field in (False, True):
+        ctx = api.Context(0)
+        ctx.set_mesh(cp.mesh, cp.tau)
+        ctx.build_dofs(cp.fixed)
+        ctx.set_material(mat)
+        if field:
+            H = np.stack([np.array(list(mat.h1)).reshape(3, 3), np.array(list(mat.h2)).reshape(3, 3)])
+            ctx.set_fiber_field(np.tile(H, (cp.mesh.n_tets, 1, 1, 1)))
+        ctx.set_loads((0.0, 0.0, 0.0), cp.load_facets, cp.load_third, cp.traction_h())
+        ctx.set_state(st)
+        rm, rp = ctx.assemble_residuals()
+        ctx.assemble_tangent(cp.ts)
+        outs.append((rm, rp, [ctx.tangent_plane(k).val for k in range(4)]))
+        ctx.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    for a, b in zip(outs[0][2], outs[1][2]):
+        assert np.array_equal(a, b)
+
+
+def test_cylinder_local_fiber_assembly_matches_restatement():
+    """Residuals and all four tangent planes on the thick-walled cylinder with per-element
+    circumferential fibre frames (HGO parameters of BASELINE configs[3]) against the restatement."""
+    from oracle import restate
+    from paper_1809_06350_b200 import CylinderProblem
+    cy = CylinderProblem(n_r=2, n_theta=16, n_z=6)
+    mesh, dofs, mat, loads, ts = _restate_cylinder(cy)
+    st = _strained_cylinder_state(cy)
+    sd = dict(u=st.u, udot=st.udot, p=st.p, pdot=st.pdot, v=st.v, vdot=st.vdot)
+    ctx = cy.context(0)
+    ctx.set_state(st)
+    rm, rp = ctx.assemble_residuals()
+    rmr, rpr = restate.assemble_residuals(mesh, dofs, mat, cy.tau, loads, sd)
+    assert np.max(np.abs(rm - rmr)) <= 1e-12 * np.max(np.abs(rmr))
+    assert np.max(np.abs(rp - rpr)) <= 1e-12 * np.max(np.abs(rpr))
+    # the fibres matter: the isotropic ground matrix alone gives a different residual
+    rm0, _ = restate.assemble_residuals(mesh, dofs, dict(mat, H=[]), cy.tau, loads, sd)
+    assert np.max(np.abs(rm0 - rmr)) > 1e-3 * np.max(np.abs(rmr))
+    ctx.assemble_tangent(cy.ts)
+    planes = restate.assemble_tangent(mesh, dofs, mat, cy.tau, loads, sd, ts)
+    for k in range(4):
+        g = ctx.tangent_plane(k).to_scipy()
+        assert abs(g - planes[k]).max() <= 1e-12 * abs(planes[k]).max(), k
+    ctx.close()
+
+
+def test_prescribed_displacement_steps_match_restatement(parity_log):
+    """Two generalized-alpha steps of the cylinder tensile test (top end displaced 1 % of the
+    length per step through ed_set_prescribed_displacement): Newton counts, residual histories,
+    accumulated linear counts and the final state against the restated step."""
+    from oracle import restate
+    from paper_1809_06350_b200 import CylinderProblem
+    cy = CylinderProblem(n_r=2, n_theta=16, n_z=6)
+    mesh, dofs, mat, loads, ts = _restate_cylinder(cy)
+    N = cy.mesh.n_nodes
+    sd = {k: np.zeros(3 * N) for k in ("u", "udot", "v", "vdot")}
+    sd.update(p=np.zeros(N), pdot=np.zeros(N))
+    kw = dict(outer=(200, 200, 1e-6), ta=(500, 500, 1e-2), ts=(200, 200, 1e-2), ti=(500, 500, 1e-2))
+    ctx = cy.context(0)
+    ctx.set_state(api.State.zeros(N))
+    opts = cy.solver_options()
+    for k in (1, 2):
+        ut = cy.top_displacement(k)
+        ctx.set_prescribed_displacement(cy.top_nodes, ut)
+        g = ctx.step(cy.ts, opts, tol_r=1e-8, tol_a=1e-6, l_max=20)
+        sd, r = restate.step_generalized_alpha(mesh, dofs, mat, cy.tau, loads, sd, ts, kw,
+                                               prescribed=(cy.top_nodes, ut))
+        sg = ctx.get_state()
+        state_err = {key: float(_rel(getattr(sg, key), sd[key])) for key in ("u", "udot", "p", "pdot", "v", "vdot")}
+        r["linear"]["converged"] = g["linear"]["converged"]
+        _record(parity_log, f"cylinder_prescribed_step{k}", g["linear"], r["linear"], g["res_history"],
+                r["res_history"], newton=[g["newton_iters"], r["newton_iters"]], state_rel=state_err,
+                oracle="restatement")
+        assert bool(g["converged"]) and r["converged"]
+        assert g["newton_iters"] == r["newton_iters"]
+        for key in COUNTERS:
+            assert abs(g["linear"][key] - r["linear"][key]) <= 1, (key, g["linear"], r["linear"])
+        h0 = r["res_history"][0]
+        assert len(g["res_history"]) == len(r["res_history"])
+        for a, b in zip(g["res_history"], r["res_history"]):
+            assert abs(a - b) <= 1e-8 * b + HIST_FLOOR * h0
+        for key, e in state_err.items():
+            assert e < X_TOL, (k, key, e)
+        top = sg.u.reshape(-1, 3)[cy.top_nodes]
+        assert np.array_equal(top, ut)
+    # a free node cannot be prescribed; a pending prescription is one-shot
+    free_node = int(np.nonzero(~cy.fixed[:, 0])[0][0])
+    with pytest.raises(ValueError):
+        ctx.set_prescribed_displacement([free_node], np.zeros((1, 3)))
+    ctx.close()
+
+
+def test_prescribing_the_current_boundary_state_is_the_homogeneous_step():
+    """Prescribing u_t = u_n at nodes at rest leaves the step bitwise the homogeneous one."""
+    cp = CubeProblem(n=6, nu=0.4)
+    st = cp.seeded_state()
+    fixed_nodes = np.nonzero(cp.fixed[:, 0])[0].astype(np.int32)
+    outs = []
+    for prescribe in (False, True):
+        ctx = cp.context(0)
+        ctx.set_state(st)
+        if prescribe:
+            ctx.set_prescribed_displacement(fixed_nodes, st.u.reshape(-1, 3)[fixed_nodes])
+        g = ctx.step(cp.ts, cp.solver_options())
+        outs.append((g, ctx.get_state()))
+        ctx.close()
+    assert outs[0][0]["newton_iters"] == outs[1][0]["newton_iters"]
+    assert np.array_equal(outs[0][0]["res_history"], outs[1][0]["res_history"])
+    for key in ("u", "udot", "p", "pdot", "v", "vdot"):
+        assert np.array_equal(getattr(outs[0][1], key), getattr(outs[1][1], key)), key

@@ -269,3 +269,78 @@ def test_reference_side_cpp_binding_builds():
         pytest.skip("reference headers absent and no prebuilt binding")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 2 and "no CUDA device" in r.stdout, (r.returncode, r.stdout, r.stderr)
+
+
+# ------------------------------------------------ cfg-3 enablers
+SOLVER_KW = dict(outer=(200, 200, 1e-6), ta=(500, 500, 1e-2), ts=(200, 200, 1e-2), ti=(500, 500, 1e-2))
+
+
+def test_restated_time_step_matches_reference():
+    """restate.step_generalized_alpha (timeint.cpp:40-180 restated) against the compiled reference:
+    two steps of the seeded 3^3 cube -- Newton counts, residual histories, linear counts, final state.
+    This pins the restated step that the prescribed-displacement GPU test compares with."""
+    cp, P, st = _setup(3, 0.4)
+    mesh, dofs, mat, tau, loads, sd, ts = _restate_problem(cp, P, st)
+    opts = ref.SolverOptions.from_buffer_copy(bytes(cp.solver_options()))
+    for k in range(2):
+        r = P.step(opts, tol_r=1e-8, tol_a=1e-6, l_max=20, t_n=k * cp.dt)
+        sd, g = R.step_generalized_alpha(mesh, dofs, mat, tau, loads, sd, ts, SOLVER_KW)
+        assert g["converged"] == bool(r["converged"])
+        assert g["newton_iters"] == r["newton_iters"]
+        for key in ("outer_iters", "a_solves", "a_iters", "s_solves", "s_iters", "schur_applies", "inner_iters"):
+            assert abs(g["linear"][key] - r["linear"][key]) <= 1, key
+        n = len(r["res_history"])
+        assert len(g["res_history"]) == n
+        h0 = r["res_history"][0]
+        for a, b in zip(g["res_history"], r["res_history"]):
+            assert abs(a - b) <= 1e-8 * b + 1e-13 * h0
+        sr = P.get_state()
+        for key in ("u", "udot", "p", "pdot", "v", "vdot"):
+            assert np.linalg.norm(sd[key] - sr[key]) <= 1e-8 * max(np.linalg.norm(sr[key]), 1e-300), key
+
+
+def test_cylinder_mesh_is_a_conforming_tube():
+    """generate_cylinder_mesh (cfg-3 geometry; the reference has boxes only, mesh.hpp:52-60):
+    positive volumes summing to the polygonal tube, conforming across the periodic seam, facet tags."""
+    from collections import Counter
+    from paper_1809_06350_b200.mesh import FACE, circumferential_fiber_dirs, generate_cylinder_mesh
+    nr, nt, nz, ri, th, L = 2, 12, 3, 1.0, 0.1, 0.5
+    m = generate_cylinder_mesh(nr, nt, nz, ri, th, L)
+    assert m.n_nodes == (nr + 1) * nt * (nz + 1) and m.n_tets == 6 * nr * nt * nz
+    assert (m.volume > 0).all()
+    ring = 0.5 * nt * np.sin(2 * np.pi / nt) * ((ri + th) ** 2 - ri ** 2)
+    assert m.volume.sum() == pytest.approx(ring * L, rel=1e-13)
+    np.testing.assert_allclose(m.grad_n.sum(axis=1), 0.0, atol=1e-11)
+    faces = Counter(map(tuple, np.sort(m.tets[:, FACE].reshape(-1, 3), axis=1)))
+    assert set(faces.values()) == {1, 2}
+    assert sum(1 for c in faces.values() if c == 1) == len(m.facet_nodes)
+    for tag, area in (("zmin", ring), ("zmax", ring), ("rmin", 2 * nt * ri * np.sin(np.pi / nt) * L)):
+        assert m.facet_area(m.facets_with_tag(m.tag_id(tag))).sum() == pytest.approx(area, rel=1e-12)
+    d = circumferential_fiber_dirs(m, 49.98)
+    np.testing.assert_allclose(np.linalg.norm(d, axis=-1), 1.0, atol=1e-15)
+    c = m.nodes[m.tets].mean(axis=1)
+    radial = c[:, :2] / np.linalg.norm(c[:, :2], axis=1)[:, None]
+    assert np.abs(np.einsum("efi,ei->ef", d[:, :, :2], radial)).max() < 1e-15  # fibres lie in the tangent plane
+    np.testing.assert_allclose(d[:, 0, 2], np.sin(np.deg2rad(49.98)), atol=1e-15)
+    np.testing.assert_allclose(d[:, 1, 2], -np.sin(np.deg2rad(49.98)), atol=1e-15)
+
+
+def test_restated_uniform_fiber_field_equals_global_fibers():
+    """A per-element fibre field whose every entry is the global structure tensor gives the
+    reference-pinned global-fibre assembly (ties the extension to materials.cpp:67-80)."""
+    p = _fiber_params(3)
+    P = ref.RefProblem(p)
+    cp = CubeProblem(n=3, nu=0.5)
+    st = cp.seeded_state()
+    st.u *= 20.0
+    P.set_state(st.u, st.udot, st.p, st.pdot, st.v, st.vdot)
+    mesh, dofs, _, tau, loads, sd, ts = _restate_problem(cp, P, st)
+    mat = _fiber_restate_mat(p)
+    E = mesh["tets"].shape[0]
+    mat_e = dict(mat, H=[np.tile(H, (E, 1, 1)) for H in mat["H"]])
+    for a, b in zip(R.assemble_residuals(mesh, dofs, mat, tau, loads, sd),
+                    R.assemble_residuals(mesh, dofs, mat_e, tau, loads, sd)):
+        assert np.array_equal(a, b)
+    for a, b in zip(R.assemble_tangent(mesh, dofs, mat, tau, loads, sd, ts),
+                    R.assemble_tangent(mesh, dofs, mat_e, tau, loads, sd, ts)):
+        assert abs(a - b).max() <= 1e-15 * abs(a).max()
