@@ -58,7 +58,9 @@ def parse():
     ap.add_argument("--spmv-n", type=int, default=160,
                     help="cube size of the 160^3 leg (the metric's BSR SpMV GB/s, assembly, Newton pass); 0 skips it")
     ap.add_argument("--big-dt", type=float, default=1e-2, help="time step of the 160^3 leg")
-    ap.add_argument("--big-newton", type=int, default=1, help="time one whole first Newton pass at 160^3 (0: skip)")
+    ap.add_argument("--big-newton", type=int, default=1,
+                    help="whole first Newton passes timed at 160^3 (0: skip; 1: one pass, which also builds the "
+                         "mesh-static solver structures; 2: a warm-up pass first)")
     a = ap.parse_args()
     cfg = {0: (10, 0.4, 1e-3), 1: (40, 0.5, 1e-3), 2: (100, 0.45, 0.1), 4: (160, 0.5, 0.1)}[a.config]
     a.n = a.n or cfg[0]
@@ -268,7 +270,7 @@ def cube_leg(n, dt, device, peak, newton):
         ctx.set_state(st)
         ctx.state_save()
         passes = []
-        for rep in range(2):
+        for rep in range(max(1, int(newton))):
             ctx.state_restore()
             ctx.timer_start()
             o = ctx.newton_first_pass(cp.ts, opts)
@@ -276,7 +278,8 @@ def cube_leg(n, dt, device, peak, newton):
             passes.append({"ms": ms, "stats": o["stats"], "norm": o["norm"], "history": [float(h) for h in o["history"]],
                            "phase_ms": o["times"]})
         last = passes[-1]
-        out["newton"] = {"solves_per_s": 1e3 / last["ms"], "pass_ms": last["ms"], "warm_pass_ms": passes[0]["ms"],
+        out["newton"] = {"solves_per_s": 1e3 / last["ms"], "pass_ms": last["ms"],
+                         "warm_pass_ms": passes[0]["ms"] if len(passes) > 1 else None,
                          "stats": last["stats"], "norm": last["norm"], "history": last["history"],
                          "phase_ms": last["phase_ms"],
                          "note": "device-timed first corrector pass (residual, tangent, both AMG setups, nested "
@@ -290,9 +293,9 @@ def cube_leg(n, dt, device, peak, newton):
 
 # FP64 flops per element of the tangent (element kernel + fold-in) and the
 # residual kernels: ncu sm__sass_thread_inst_executed_op_{dadd,dmul,dfma}
-# (fma = 2) of one launch over its elements (profiles/r01c_assembly_ncu.md)
-TANGENT_FLOP_PER_ELEM = None
-RESIDUAL_FLOP_PER_ELEM = None
+# (fma = 2) of every colour launch of one pass over its elements (profiles/r02/assembly_fp64_ncu.md)
+TANGENT_FLOP_PER_ELEM = 21298.0
+RESIDUAL_FLOP_PER_ELEM = 1632.5
 
 
 def assembly_row(a, peak):
