@@ -385,6 +385,23 @@ std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLay
     S.sync.alloc(static_cast<size_t>(std::max(nlev, 1)) + 2);
     S.sync.zero(s);
     S.d_lev_ptr.upload(S.lev_ptr, s);
+    // structural symmetry (sorted columns): every later neighbour of a row waits on that row, which is
+    // what lets the tagged dataflow sweep read later neighbours' old values without a level barrier
+    S.sym_pattern = false;
+    if (S.leveled && pat.nbr == pat.nbc) {
+        int asym = 0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(+ : asym)
+        for (int r = 0; r < n; ++r)
+            for (int64_t k = pat.rowptr[r]; k < pat.rowptr[r + 1]; ++k) {
+                const int c = pat.col[k];
+                if (c == r) continue;
+                const int* b0 = pat.col.data() + pat.rowptr[c];
+                const int* b1 = pat.col.data() + pat.rowptr[c + 1];
+                const int* it = std::lower_bound(b0, b1, r);
+                if (it == b1 || *it != r) ++asym;
+            }
+        S.sym_pattern = asym == 0;
+    }
     // narrow level schedules (every level fits one 512-thread CTA in <= 2 passes) run as one CTA
     int widest = 0;
     for (int l = 0; l < nlev; ++l) widest = std::max(widest, S.lev_ptr[l + 1] - S.lev_ptr[l]);

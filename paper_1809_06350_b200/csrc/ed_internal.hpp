@@ -183,6 +183,10 @@ struct BsrStruct {
     DevArray<int> item_level; // [nitems]
     DevArray<int> lev_items;  // [nlev] items per level
     DevArray<unsigned int> sync; // [nlev + 2]: per-level done counters, ticket
+    // tagged dataflow sweep (k_sgs_tag): z entries published as {lo32, epoch}{hi32, epoch} words
+    mutable DevArray<ulonglong2> ztag; // [nbr * Rb], allocated zeroed at the first sweep
+    mutable unsigned int tag_epoch = 0; // last epoch used (one per half sweep)
+    bool sym_pattern = false;           // structurally symmetric (the tagged sweep's precondition)
     bool chain = false;          // narrow levels: single-CTA sweep with CTA barriers
     int avg_rows_per_level = 0;
     DevArray<int> d_lev_ptr;     // device copy of lev_ptr

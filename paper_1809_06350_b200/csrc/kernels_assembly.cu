@@ -655,7 +655,7 @@ void launch_k4_split(const double* k4, const int* dstA, const int* dstB, const i
 // ED_ASM_MINB=<residual><tangent> picks a variant (experiments), e.g. 86
 int asm_minb(int which)
 {
-    // measured at 160^3 (profiles/r01c_assembly.md): residual 8 CTAs/SM (64
+    // measured at 160^3 (round-1 ED_ASM_MINB scan with scripts/asm_probe.py): residual 8 CTAs/SM (64
     // registers), tangent 4 (128 registers, no spills)
     const char* e = std::getenv("ED_ASM_MINB");
     const int v = e ? std::atoi(e) : 84;

@@ -356,24 +356,43 @@ __global__ void __launch_bounds__(128) k_group_tinv(GrpArgs a, const double* __r
         const int cr = FWD ? cl : B - 1 - cl;
         const int row = a.perm ? a.perm[sr] : sr;
         double acc = (i == j) ? 1.0 : 0.0;
-        for (int q = a.gptr[sr]; q < a.gptr[sr + 1]; ++q) {
-            const int k = a.gblk[q];
-            const int code = a.bcode[k];
-            const int c = a.col[k];
-            const int sc = a.inv ? a.inv[c] : c;
-            const double* vp = a.val + static_cast<int64_t>(k) * (B * B) + cr * B;
-            if (code == 3) {
+        // The row's in-group blocks: the index chain (block -> code, column -> stored row) is
+        // resolved for 32 blocks at once, one per lane, then the blocks are applied in order
+        // (the same subtraction order as a lane-serial loop) with their operands broadcast.
+        const int q0 = a.gptr[sr], q1 = a.gptr[sr + 1];
+        for (int qb = q0; qb < q1; qb += 32) {
+            int mk = 0, mcode = 0, msc = 0;
+            if (qb + lane < q1) {
+                mk = a.gblk[qb + lane];
+                mcode = a.bcode[mk];
+                const int c = a.col[mk];
+                msc = a.inv ? a.inv[c] : c;
+            }
+            const int nb = min(32, q1 - qb);
+            for (int e = 0; e < nb; ++e) {
+                const int k = __shfl_sync(0xffffffffu, mk, e);
+                const int code = __shfl_sync(0xffffffffu, mcode, e);
+                const int sc = __shfl_sync(0xffffffffu, msc, e);
+                const double* vp = a.val + static_cast<int64_t>(k) * (B * B) + cr * B;
+                if (code == 3) {
 #pragma unroll
-                for (int d = 0; d < B; ++d) {
-                    if (!(FWD ? d < cr : d > cr)) continue;
-                    const int kl = local_of<B, FWD>(sr, d, r0, r1);
-                    if (j <= kl) acc -= vp[d] * Xg[static_cast<int64_t>(kl) * (kl + 1) / 2 + j];
-                }
-            } else if (code == (FWD ? 1 : 2)) {
+                    for (int d = 0; d < B; ++d) {
+                        if (!(FWD ? d < cr : d > cr)) continue;
+                        const int kl = local_of<B, FWD>(sr, d, r0, r1);
+                        if (j <= kl) acc -= vp[d] * Xg[static_cast<int64_t>(kl) * (kl + 1) / 2 + j];
+                    }
+                } else if (code == (FWD ? 1 : 2)) {
+                    double xs[B];
 #pragma unroll
-                for (int d = 0; d < B; ++d) {
-                    const int kl = local_of<B, FWD>(sc, d, r0, r1);
-                    if (j <= kl) acc -= vp[d] * Xg[static_cast<int64_t>(kl) * (kl + 1) / 2 + j];
+                    for (int d = 0; d < B; ++d) {
+                        const int kl = local_of<B, FWD>(sc, d, r0, r1);
+                        xs[d] = j <= kl ? Xg[static_cast<int64_t>(kl) * (kl + 1) / 2 + j] : 0.0;
+                    }
+#pragma unroll
+                    for (int d = 0; d < B; ++d) {
+                        const int kl = local_of<B, FWD>(sc, d, r0, r1);
+                        if (j <= kl) acc -= vp[d] * xs[d];
+                    }
                 }
             }
         }

@@ -328,6 +328,177 @@ __global__ void __launch_bounds__(kThreads, 2) k_sgs_flow(BsrArgs m, const doubl
     }
 }
 
+
+// ---- tagged dataflow sweep ------------------------------------------------
+// A z entry is published as two 8-byte words {low half, epoch} {high half,
+// epoch} (8-byte accesses are single-copy atomic, so a word whose tag equals
+// this half sweep's epoch carries this half sweep's value: no flag, no fence and
+// no second round trip between "the producer is done" and "its value is
+// here").  A row waits only on the neighbours that precede it in the sweep
+// (original index smaller in a forward sweep, larger in a backward sweep: the
+// reference's in-place loop, amg.cpp:311-322); later neighbours are read from
+// the plain z, which their owners overwrite only after consuming this row's
+// tagged value (structurally symmetric pattern, BsrStruct::sym_pattern).
+__device__ __forceinline__ void st_tagged(ulonglong2* p, double v, unsigned int tag)
+{
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    const unsigned long long t = static_cast<unsigned long long>(tag) << 32;
+    const unsigned long long w0 = (b & 0xffffffffull) | t, w1 = (b >> 32) | t;
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
+}
+
+__device__ __forceinline__ bool ld_tagged(const ulonglong2* p, unsigned int tag, double& v)
+{
+    unsigned long long w0, w1;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+    v = __longlong_as_double(static_cast<long long>((w0 & 0xffffffffull) | (w1 << 32)));
+    return static_cast<unsigned int>(w0 >> 32) == tag && static_cast<unsigned int>(w1 >> 32) == tag;
+}
+
+// NQ blocks per lane: columns c[q] (-1: none), row `row`.  Entries of the
+// neighbours that precede the row in the sweep are polled until their tags
+// carry this epoch (all lanes of the warp iterate together); the others come
+// from the plain z.  (Measured alternatives, profiles/r02/sweeps.md: polling
+// one sentinel word per row first, re-polling only the missing values, and a
+// frontier hint for far-ahead warps were all slower.)
+template <int B, int NQ, bool FWD>
+__device__ __forceinline__ void gather_tagged(const int (&c)[NQ], int row, const double* z, const ulonglong2* zt,
+                                              unsigned int epoch, double (&zv)[NQ][B])
+{
+    bool fresh[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        fresh[q] = c[q] >= 0 && (FWD ? c[q] < row : c[q] > row);
+        const int64_t cc = c[q] >= 0 ? c[q] : 0;
+#pragma unroll
+        for (int d = 0; d < B; ++d) zv[q][d] = fresh[q] ? 0.0 : __ldcg(z + cc * B + d);
+    }
+    for (;;) {
+        bool ok = true;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            if (!fresh[q]) continue;
+#pragma unroll
+            for (int d = 0; d < B; ++d) ok = ld_tagged(zt + static_cast<int64_t>(c[q]) * B + d, epoch, zv[q][d]) && ok;
+        }
+        if (__all_sync(0xffffffffu, ok)) break;
+        __nanosleep(40);
+    }
+}
+
+template <int B, int L, int PF, bool FWD>
+__device__ __forceinline__ void finish_row_tagged(const BsrArgs& m, double* z, ulonglong2* zt, unsigned int epoch,
+                                                  bool valid, int lane, const RowPref<B, PF>& P)
+{
+    double acc[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) acc[r] = 0.0;
+    {
+        double zv[PF][B];
+        gather_tagged<B, PF, FWD>(P.c, P.row, z, zt, epoch, zv);
+#pragma unroll
+        for (int q = 0; q < PF; ++q) {
+            const bool use = P.c[q] >= 0 && P.c[q] != P.row;
+#pragma unroll
+            for (int d = 0; d < B; ++d)
+#pragma unroll
+                for (int r = 0; r < B; ++r) acc[r] = use ? fma(P.v[q][r * B + d], zv[q][d], acc[r]) : acc[r];
+        }
+    }
+    // long rows: the rest in batches of NB blocks per lane (warp-uniform trip count)
+    constexpr int NB = B == 3 ? 2 : 8;
+    int more = 0;
+    for (int k0 = P.kb + PF * L; k0 < P.ke; k0 += NB * L) ++more;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) more = max(more, __shfl_xor_sync(0xffffffffu, more, o));
+    for (int it = 0; it < more; ++it) {
+        const int k0 = P.kb + (PF + it * NB) * L;
+        int cb[NB];
+        double vb[NB][B * B], zb[NB][B];
+#pragma unroll
+        for (int p = 0; p < NB; ++p) {
+            const int k = k0 + p * L;
+            const bool in = k < P.ke;
+            cb[p] = in ? __ldg(m.col + k) : -1;
+#pragma unroll
+            for (int e = 0; e < B * B; ++e) vb[p][e] = in ? __ldg(m.val + static_cast<int64_t>(k) * (B * B) + e) : 0.0;
+        }
+        gather_tagged<B, NB, FWD>(cb, P.row, z, zt, epoch, zb);
+#pragma unroll
+        for (int p = 0; p < NB; ++p) {
+            const bool use = cb[p] >= 0 && cb[p] != P.row;
+#pragma unroll
+            for (int d = 0; d < B; ++d)
+#pragma unroll
+                for (int r = 0; r < B; ++r) acc[r] = use ? fma(vb[p][r * B + d], zb[p][d], acc[r]) : acc[r];
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < B; ++r) acc[r] = group_sum<L>(acc[r]);
+    if (valid && lane == 0) {
+        double zs[B];
+#pragma unroll
+        for (int d = 0; d < B; ++d) zs[d] = P.zs[d];
+#pragma unroll
+        for (int ci = 0; ci < B; ++ci) {
+            const int c = FWD ? ci : B - 1 - ci;
+            double a = P.b[c] - acc[c];
+#pragma unroll
+            for (int d = 0; d < B; ++d)
+                if (d != c) a -= P.D[c * B + d] * zs[d];
+            zs[c] = a * P.id[c];
+        }
+#pragma unroll
+        for (int d = 0; d < B; ++d) st_tagged(zt + static_cast<int64_t>(P.row) * B + d, zs[d], epoch);
+#pragma unroll
+        for (int d = 0; d < B; ++d) z[static_cast<int64_t>(P.row) * B + d] = zs[d];
+    }
+}
+
+// One Gauss-Seidel half sweep, tagged dataflow.  Work items are 32/L rows of
+// one level; every WARP takes items in level order from a ticket counter (the
+// next ticket is taken before the current item is processed, so the atomic's
+// latency is hidden): no CTA barrier and no level counter.  Deadlock-free under
+// any residency: a row only waits on rows of earlier tickets, tickets are only
+// held by running warps, and a warp works through its tickets in order.
+template <int B, int L, bool FWD>
+__global__ void __launch_bounds__(kThreads, 2) k_sgs_tag(BsrArgs m, const double* __restrict__ bvec, double* z,
+                                                      ulonglong2* zt, unsigned int epoch,
+                                                      const double* __restrict__ invd, int nitems,
+                                                      const int* __restrict__ item_row, unsigned int* ticket)
+{
+    constexpr int PF = (B == 3) ? 3 : 4;
+    constexpr int WPI = kThreads / 32; // warp items per table item (items hold <= kThreads / L rows)
+    constexpr int RPW = 32 / L;        // rows per warp item
+    const int lane32 = threadIdx.x & 31;
+    const int g = lane32 / L;
+    const int lane = lane32 % L;
+    const int nw = nitems * WPI;
+    auto take = [&]() {
+        unsigned int t = 0;
+        if (lane32 == 0) t = atomicAdd(ticket, 1u);
+        return static_cast<int>(__shfl_sync(0xffffffffu, t, 0));
+    };
+    int t = take();
+    while (t < nw) {
+        const int tn = take();
+        const int tt = FWD ? t : nw - 1 - t;
+        const int item = tt / WPI;
+        const int s = item_row[item] + (tt % WPI) * RPW + g;
+        const bool valid = s < item_row[item + 1];
+        if (__any_sync(0xffffffffu, valid)) {
+            RowPref<B, PF> P;
+            prefetch_row<B, L, PF>(m, bvec, invd, z, s, valid, lane, P);
+            if (!valid) {
+#pragma unroll
+                for (int q = 0; q < PF; ++q) P.c[q] = -1;
+            }
+            finish_row_tagged<B, L, PF, FWD>(m, z, zt, epoch, valid, lane, P);
+        }
+        t = tn;
+    }
+}
+
 template <int B, int L, bool FWD>
 __global__ void __launch_bounds__(512) k_sgs_chain(BsrArgs m, const double* __restrict__ bvec, double* z,
                                                     const double* __restrict__ invd, const int* __restrict__ lev_ptr,
@@ -477,6 +648,36 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
                 k_sgs_chain<B, LL, false><<<1, 512, 0, s>>>(a, b, z, invd, S.d_lev_ptr.p, nlev);
         })
         after_launch("k_sgs_chain");
+        return;
+    }
+    // structurally symmetric operators: the tagged dataflow sweep (ED_FLOW_LEGACY=1: level counters)
+    static const bool tagged = std::getenv("ED_FLOW_LEGACY") == nullptr;
+    if (tagged && S.sym_pattern) {
+        if (S.ztag.n != static_cast<size_t>(S.nbr) * B) {
+            S.ztag.alloc(static_cast<size_t>(S.nbr) * B);
+            S.ztag.zero(s);
+            S.tag_epoch = 0;
+        }
+        if (++S.tag_epoch == 0) { // epoch wrap: start over from clean tags
+            S.ztag.zero(s);
+            S.tag_epoch = 1;
+        }
+        ED_CUDA(cudaMemsetAsync(S.sync.p, 0, sizeof(unsigned int), s)); // the ticket
+        // eight levels' worth of warps (measured best of 1..16 at 40^3, profiles/r02/sweeps.md): fewer
+        // cannot hide an item's ticket + matrix-prefetch latency, more only add polling traffic
+        const int64_t per_level = (static_cast<int64_t>(S.nitems) * (kThreads / 32) + nlev - 1) / std::max(nlev, 1);
+        static const int lv_ahead = std::getenv("ED_TAG_AHEAD") ? std::atoi(std::getenv("ED_TAG_AHEAD")) : 8;
+        const int tgrid =
+            static_cast<int>(std::min<int64_t>(148 * 2, std::max<int64_t>(1, (lv_ahead * per_level + 7) / 8)));
+        ED_LANES(S.Ls, {
+            if (fwd)
+                k_sgs_tag<B, LL, true><<<tgrid, kThreads, 0, s>>>(a, b, z, S.ztag.p, S.tag_epoch, invd, S.nitems,
+                                                                 S.item_row.p, S.sync.p);
+            else
+                k_sgs_tag<B, LL, false><<<tgrid, kThreads, 0, s>>>(a, b, z, S.ztag.p, S.tag_epoch, invd, S.nitems,
+                                                                  S.item_row.p, S.sync.p);
+        })
+        after_launch("k_sgs_tag");
         return;
     }
     ED_CUDA(cudaMemsetAsync(S.sync.p, 0, S.sync.n * sizeof(unsigned int), s));
