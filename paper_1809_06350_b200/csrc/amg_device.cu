@@ -946,23 +946,17 @@ Bsr bsr_leveled(const DBsrRaw& m, cudaStream_t s, LevelCache* cache)
     int nlev = 0;
     gs_level_order(pat, order, lvl, nlev);
     lap("levels");
-    // the push sweep's ring layout only where the group sweep will not run (bsr_host.cpp: grp_use)
-    static const int grp_rpl = std::getenv("ED_GROUP_MAX_RPL") ? std::atoi(std::getenv("ED_GROUP_MAX_RPL")) : 64;
-    const bool grouped = sweep_mode() != 1 && nlev > 0 && static_cast<double>(m.nbr) / nlev <= grp_rpl;
-    const int rcs = m.Rb == m.Cb && !grouped ? ring_order(pat, m.Rb, order, lvl, nlev) : 0;
-    lap("ring order");
     BsrLayout lay = make_layout(pat, order, lvl);
-    lay.ring_cs = rcs;
     lap("layout");
     out.st = bsr_make_struct(pat, lay, m.Rb, m.Cb, s);
     lap("struct");
     out.st->leveled = true;
     if (std::getenv("ED_AMG_VERBOSE"))
         std::fprintf(stderr,
-                     "[amg-dev] level op: block rows %d blocks %lld gs-levels %d lanes %d push %d groups %d (%s) "
+                     "[amg-dev] level op: block rows %d blocks %lld gs-levels %d lanes %d groups %d (%s) "
                      "(%.1f ms host)\n",
-                     m.nbr, static_cast<long long>(m.nnzb), out.st->nlev(), out.st->L, out.st->ring_cs, out.st->ngrp,
-                     group_sweep_on(*out.st) ? "group sweep" : "legacy sweep", now_ms_host() - t_start);
+                     m.nbr, static_cast<long long>(m.nnzb), out.st->nlev(), out.st->L, out.st->ngrp,
+                     group_sweep_on(*out.st) ? "group sweep" : "tagged dataflow sweep", now_ms_host() - t_start);
     out.val.alloc(std::max<int64_t>(m.nnzb * E, 1));
     k_gather_rows<<<g1(m.nbr), kT, 0, s>>>(m.rowptr, m.val, out.st->perm.p ? out.st->perm.p : nullptr, m.nbr, E,
                                            out.st->rowptr.p, out.val.p);

@@ -45,234 +45,6 @@ void gs_level_order(const BlockPattern& pat, std::vector<int>& order, std::vecto
     }
 }
 
-namespace {
-constexpr int kRingSliceMaxBytes = 40 * 1024; // z slice per CTA (b and inv_diag slices alongside)
-constexpr int kRingPartMaxBytes = 24 * 1024;  // one partial-sum slot per CTA
-constexpr int kRingMinRows = 4096;            // smaller operators: group / chain sweeps, dense tail
-
-int64_t push_chunk_bytes(int64_t m, int64_t pk0, int64_t pk1, int64_t s0, int64_t nown, int B)
-{
-    const int64_t BB = B * B;
-    const int64_t cb = 4 * (((pk1 + 3) & ~int64_t(3)) - (pk0 & ~int64_t(3)));
-    const int64_t vb = 8 * BB * (((pk1 + 1) & ~int64_t(1)) - (pk0 & ~int64_t(1)));
-    const int64_t db = 8 * BB * (((s0 + nown + 1) & ~int64_t(1)) - (s0 & ~int64_t(1)));
-    return 16 * m + cb + vb + db;
-}
-
-// Rows of level l are dealt round-robin starting at CTA l % cs (row q -> CTA
-// (q + l) % cs) and stored CTA-major; rows CTA c gets at level l:
-inline int dealt(int m, int c, int l, int cs)
-{
-    const int first = ((c - l) % cs + cs) % cs; // smallest q with (q + l) % cs == c
-    return first < m ? (m - 1 - first) / cs + 1 : 0;
-}
-constexpr int kRingSlots = 4; // partial-sum slots (kernels_ring.cu)
-constexpr int kRingScratchMaxBytes = 32 * 1024; // push_scratch_bytes limit
-
-// Forced cluster barriers of the push sweep: slot (i mod K) of a CTA is
-// reused every K levels, so a CTA may push level-i partials only once every
-// peer finished level i-K.  A CTA that waited for its own rows' partials at
-// level k knows every peer finished k-1; where some CTA went K-1 levels
-// without owning a row, a cluster barrier before the level resets all.
-// bit 0: forward sweep, bit 1: backward sweep (sequence order reversed).
-std::vector<int> push_barriers(const std::vector<int>& lev_ptr, int cs)
-{
-    const int L = static_cast<int>(lev_ptr.size()) - 1;
-    std::vector<int> flags(L, 0);
-    for (int dir = 0; dir < 2; ++dir) {
-        std::vector<int> last(cs, 0); // the kernel-start cluster barrier
-        for (int i = 0; i < L; ++i) {
-            const int l = dir == 0 ? i : L - 1 - i;
-            const int m = lev_ptr[l + 1] - lev_ptr[l];
-            bool need = false;
-            for (int c = 0; c < cs; ++c) need = need || i - last[c] > kRingSlots - 1;
-            if (need) {
-                flags[l] |= 1 << dir;
-                std::fill(last.begin(), last.end(), i);
-            }
-            for (int c = 0; c < cs; ++c)
-                if (dealt(m, c, l, cs) > 0) last[c] = i;
-        }
-    }
-    return flags;
-}
-} // namespace
-
-int ring_order(const BlockPattern& pat, int B, std::vector<int>& order, const std::vector<int>& level_of_pos, int nlev)
-{
-    static const bool off = std::getenv("ED_NO_RING") != nullptr;
-    const int n = pat.nbr;
-    if (off || (B != 1 && B != 3) || nlev < 2 || n < kRingMinRows || pat.nbr != pat.nbc) return 0;
-    const int cs = ring_cluster_size();
-    if (cs == 0) return 0;
-    std::vector<int> lev_ptr{0};
-    for (int p = 1; p < n; ++p)
-        if (level_of_pos[p] != level_of_pos[p - 1]) lev_ptr.push_back(p);
-    lev_ptr.push_back(n);
-    const int L = static_cast<int>(lev_ptr.size()) - 1;
-    std::vector<int64_t> slice(cs, 0);
-    int mown = 0;
-    for (int l = 0; l < L; ++l) {
-        const int m = lev_ptr[l + 1] - lev_ptr[l];
-        for (int c = 0; c < cs; ++c) slice[c] += dealt(m, c, l, cs);
-        mown = std::max(mown, (m + cs - 1) / cs);
-    }
-    const int64_t smax = *std::max_element(slice.begin(), slice.end());
-    const int PB = B == 3 ? 4 : 1;
-    const int part = mown * cs * PB * 8;
-    if (smax * B * 8 > kRingSliceMaxBytes || part > kRingPartMaxBytes || mown > 256) return 0;
-    // the deal: per level, CTA-major round-robin (stable in the old order)
-    std::vector<int> neworder(n), owner(n);
-    for (int l = 0; l < L; ++l) {
-        const int a = lev_ptr[l], m = lev_ptr[l + 1] - a;
-        int out = a;
-        for (int c = 0; c < cs; ++c)
-            for (int q = ((c - l) % cs + cs) % cs; q < m; q += cs) {
-                neworder[out++] = order[a + q];
-                owner[order[a + q]] = c;
-            }
-    }
-    // chunk sizes: blocks of the level's rows whose column CTA c owns
-    std::vector<int64_t> nblk(static_cast<size_t>(L) * cs, 0);
-    for (int l = 0; l < L; ++l) {
-        const int a = lev_ptr[l], m = lev_ptr[l + 1] - a;
-        for (int p = a; p < a + m; ++p) {
-            const int r = neworder[p];
-            for (int64_t k = pat.rowptr[r]; k < pat.rowptr[r + 1]; ++k)
-                if (pat.col[k] != r) ++nblk[static_cast<size_t>(l) * cs + owner[pat.col[k]]];
-        }
-    }
-    int maxm = 0;
-    for (int l = 0; l < L; ++l) maxm = std::max(maxm, lev_ptr[l + 1] - lev_ptr[l]);
-    if (push_scratch_bytes(maxm, B) > kRingScratchMaxBytes) return 0;
-    const int cap = ring_capacity(static_cast<int>(smax * B), part * kRingSlots + push_scratch_bytes(maxm, B));
-    int64_t pk = 0;
-    for (int l = 0; l < L; ++l) {
-        const int m = lev_ptr[l + 1] - lev_ptr[l];
-        int s0 = lev_ptr[l];
-        for (int c = 0; c < cs; ++c) {
-            const int nown = dealt(m, c, l, cs);
-            const int64_t nb = nblk[static_cast<size_t>(l) * cs + c];
-            if (3 * push_chunk_bytes(m, pk, pk + nb, s0, nown, B) > cap) return 0; // two chunks always fit
-            pk += nb;
-            s0 += nown;
-        }
-    }
-    order.swap(neworder);
-    return cs;
-}
-
-
-// Push-sweep structures of a ring-ordered operator (kernels_ring.cu).
-static void ring_build(BsrStruct& S, const BsrLayout& lay, cudaStream_t s)
-{
-    const int cs = lay.ring_cs, n = S.nbr, nlev = S.nlev(), B = S.Rb;
-    const int PB = B == 3 ? 4 : 1;
-    std::vector<int> owner(n), zl(n), qown(n), cnt(cs, 0), own_ptr(cs + 1, 0);
-    std::vector<std::vector<int>> own(cs);
-    std::vector<int4> chunk(static_cast<size_t>(nlev) * cs * 2);
-    const std::vector<int> flags = push_barriers(S.lev_ptr, cs);
-    int mown = 0;
-    for (int l = 0; l < nlev; ++l) {
-        const int a = S.lev_ptr[l], m = S.lev_ptr[l + 1] - a;
-        int sp = a;
-        for (int c = 0; c < cs; ++c) {
-            const int k = dealt(m, c, l, cs);
-            mown = std::max(mown, k);
-            chunk[(static_cast<size_t>(l) * cs + c) * 2 + 1] = make_int4(sp, k, cnt[c] * B, flags[l]);
-            for (int q = 0; q < k; ++q) {
-                owner[sp + q] = c;
-                zl[sp + q] = cnt[c] * B;
-                qown[sp + q] = q;
-                ++cnt[c];
-                own[c].push_back(lay.perm[sp + q]);
-            }
-            sp += k;
-        }
-    }
-    std::vector<int> rown, psrc, pcol, lev_of(n);
-    // (pk indices fit int32: checked below)
-    for (int l = 0; l < nlev; ++l)
-        for (int q = S.lev_ptr[l]; q < S.lev_ptr[l + 1]; ++q) lev_of[q] = l;
-    for (int c = 0; c < cs; ++c) {
-        own_ptr[c + 1] = own_ptr[c] + static_cast<int>(own[c].size());
-        rown.insert(rown.end(), own[c].begin(), own[c].end());
-    }
-    // packed blocks per level (off-diagonal), then every level in parallel:
-    // a counting sort of its blocks by (CTA owning the column, row, part) where
-    // part orders [columns on level l-1 | other levels | level l+1]: the first
-    // part is the forward sweep's late part, the last the backward's
-    std::vector<int64_t> lvl_pk(nlev + 1, 0);
-#pragma omp parallel for schedule(dynamic, 8)
-    for (int l = 0; l < nlev; ++l) {
-        int64_t c0 = 0;
-        for (int q = S.lev_ptr[l]; q < S.lev_ptr[l + 1]; ++q)
-            for (int k = S.h_rowptr[q]; k < S.h_rowptr[q + 1]; ++k) c0 += lay.inv[S.h_col[k]] != q;
-        lvl_pk[l + 1] = c0;
-    }
-    for (int l = 0; l < nlev; ++l) lvl_pk[l + 1] += lvl_pk[l];
-    if (lvl_pk[nlev] >= (1LL << 31)) throw Error(ED_UNSUPPORTED, "push sweep: too many blocks");
-    psrc.resize(lvl_pk[nlev]);
-    pcol.resize(lvl_pk[nlev]);
-    std::vector<int4> seg(static_cast<size_t>(n) * cs);
-    bool too_long = false;
-#pragma omp parallel for schedule(dynamic, 8) reduction(|| : too_long)
-    for (int l = 0; l < nlev; ++l) {
-        const int a = S.lev_ptr[l], m = S.lev_ptr[l + 1] - a;
-        const int K = cs * m * 3;
-        std::vector<int> start(K + 1, 0);
-        auto key = [&](int q, int k) {
-            const int sc = lay.inv[S.h_col[k]];
-            const int lc = lev_of[sc];
-            const int part_of = lc == l - 1 ? 0 : lc == l + 1 ? 2 : 1;
-            return (owner[sc] * m + (q - a)) * 3 + part_of;
-        };
-        for (int q = a; q < a + m; ++q)
-            for (int k = S.h_rowptr[q]; k < S.h_rowptr[q + 1]; ++k)
-                if (lay.inv[S.h_col[k]] != q) ++start[key(q, k) + 1];
-        for (int i = 0; i < K; ++i) start[i + 1] += start[i];
-        std::vector<int> pos(start.begin(), start.end() - 1);
-        const int64_t base = lvl_pk[l];
-        for (int q = a; q < a + m; ++q)
-            for (int k = S.h_rowptr[q]; k < S.h_rowptr[q + 1]; ++k) {
-                const int sc = lay.inv[S.h_col[k]];
-                if (sc == q) continue;
-                const int64_t at = base + pos[key(q, k)]++;
-                psrc[at] = k;
-                pcol[at] = zl[sc];
-            }
-        for (int c = 0; c < cs; ++c) {
-            chunk[(static_cast<size_t>(l) * cs + c) * 2] =
-                make_int4(cs * a + c * m, m, static_cast<int>(base + start[c * m * 3]),
-                          static_cast<int>(base + start[(c + 1) * m * 3]));
-            for (int qi = 0; qi < m; ++qi) {
-                const int kk = (c * m + qi) * 3;
-                const int na = start[kk + 1] - start[kk], nb = start[kk + 3] - start[kk + 2];
-                too_long = too_long || na > 0xFFFF || nb > 0xFFFF;
-                const int q = a + qi;
-                seg[static_cast<size_t>(cs) * a + c * m + qi] =
-                    make_int4(static_cast<int>(base + start[kk]), static_cast<int>(base + start[kk + 3]),
-                              (owner[q] << 24) | ((qown[q] * cs + c) * PB * 8), (na << 16) | nb);
-            }
-        }
-    }
-    if (too_long) throw Error(ED_UNSUPPORTED, "push sweep: row segment too long");
-    S.ring_cs = cs;
-    S.ring_slice = *std::max_element(cnt.begin(), cnt.end()) * B;
-    S.ring_part = mown * cs * PB * 8;
-    int maxm = 0;
-    for (int l = 0; l < nlev; ++l) maxm = std::max(maxm, S.lev_ptr[l + 1] - S.lev_ptr[l]);
-    S.ring_maxm = maxm;
-    S.ring_cap = ring_capacity(S.ring_slice, S.ring_part * kRingSlots + push_scratch_bytes(maxm, B));
-    S.ring_npk = static_cast<int64_t>(psrc.size());
-    S.rchunk.upload(chunk, s);
-    S.rseg.upload(seg, s);
-    S.rpcol.upload(pcol, s);
-    S.rpsrc.upload(psrc, s);
-    S.rown.upload(rown, s);
-    S.rown_ptr.upload(own_ptr, s);
-}
-
 bool pattern_symmetric(const BlockPattern& pat)
 {
     if (pat.nbr != pat.nbc) return false;
@@ -371,45 +143,20 @@ std::shared_ptr<BsrStruct> bsr_make_struct(const BlockPattern& pat, const BsrLay
     // dataflow items: rows_per_item rows of one level each (256 threads / L lanes)
     const int nlev = S.nlev();
     S.rows_per_item = 256 / S.Ls;
-    std::vector<int> irow{0}, ilev, lcnt(std::max(nlev, 1), 0);
+    std::vector<int> irow{0};
     for (int l = 0; l < nlev; ++l)
-        for (int r0 = S.lev_ptr[l]; r0 < S.lev_ptr[l + 1]; r0 += S.rows_per_item) {
+        for (int r0 = S.lev_ptr[l]; r0 < S.lev_ptr[l + 1]; r0 += S.rows_per_item)
             irow.push_back(std::min(r0 + S.rows_per_item, S.lev_ptr[l + 1]));
-            ilev.push_back(l);
-            ++lcnt[l];
-        }
-    S.nitems = static_cast<int>(ilev.size());
+    S.nitems = static_cast<int>(irow.size()) - 1;
     S.item_row.upload(irow, s);
-    S.item_level.upload(ilev, s);
-    S.lev_items.upload(lcnt, s);
-    S.sync.alloc(static_cast<size_t>(std::max(nlev, 1)) + 2);
+    S.sync.alloc(2);
     S.sync.zero(s);
     S.d_lev_ptr.upload(S.lev_ptr, s);
-    // structural symmetry (sorted columns): every later neighbour of a row waits on that row, which is
-    // what lets the tagged dataflow sweep read later neighbours' old values without a level barrier
-    S.sym_pattern = false;
-    if (S.leveled && pat.nbr == pat.nbc) {
-        int asym = 0;
-#pragma omp parallel for schedule(dynamic, 4096) reduction(+ : asym)
-        for (int r = 0; r < n; ++r)
-            for (int64_t k = pat.rowptr[r]; k < pat.rowptr[r + 1]; ++k) {
-                const int c = pat.col[k];
-                if (c == r) continue;
-                const int* b0 = pat.col.data() + pat.rowptr[c];
-                const int* b1 = pat.col.data() + pat.rowptr[c + 1];
-                const int* it = std::lower_bound(b0, b1, r);
-                if (it == b1 || *it != r) ++asym;
-            }
-        S.sym_pattern = asym == 0;
-    }
     // narrow level schedules (every level fits one 512-thread CTA in <= 2 passes) run as one CTA
     int widest = 0;
     for (int l = 0; l < nlev; ++l) widest = std::max(widest, S.lev_ptr[l + 1] - S.lev_ptr[l]);
     S.chain = static_cast<int64_t>(widest) * S.Ls <= 1024;
     S.avg_rows_per_level = nlev > 0 ? S.nbr / nlev : 0;
-    if (lay.ring_cs > 0 && Rb == Cb && pat.nbr == pat.nbc) {
-        ring_build(S, lay, s);
-    }
     if (Rb == Cb && (Rb == 1 || Rb == 3) && pat.nbr == pat.nbc && S.leveled && S.nbr > 0) group_build(S, s);
     ED_CUDA(cudaStreamSynchronize(s)); // host vectors die at return
     return st;
@@ -573,18 +320,15 @@ Bsr bsr_from_csr(const HostCsr& a, int Rb, int Cb, bool leveled, cudaStream_t s)
 {
     const BlockPattern pat = block_pattern_of_csr(a, Rb, Cb);
     std::vector<int> order, lvl;
-    int ring_cs = 0;
     if (leveled) {
         if (!pattern_symmetric(pat)) throw Error(ED_UNSUPPORTED, "Gauss-Seidel operator pattern is not symmetric");
         int nlev = 0;
         gs_level_order(pat, order, lvl, nlev);
-        ring_cs = Rb == Cb ? ring_order(pat, Rb, order, lvl, nlev) : 0;
     } else {
         order.resize(pat.nbr);
         std::iota(order.begin(), order.end(), 0);
     }
     BsrLayout lay = make_layout(pat, order, lvl);
-    lay.ring_cs = ring_cs;
     Bsr m;
     m.st = bsr_make_struct(pat, lay, Rb, Cb, s);
     if (leveled) m.st->leveled = true;

@@ -97,8 +97,7 @@ struct DevArray {
         if (count == 0) return;
         const double t0 = now_ms_host();
         as = alloc_stream();
-        // kPad bytes of slack: 16-B-granular bulk (TMA) copies may round a
-        // range's end up past the last element (kernels_ring.cu)
+        // kPad bytes of slack: 16-B vector loads may round a range's end up past the last element
         if (as) p = static_cast<T*>(cache_alloc(count * sizeof(T) + kPad, as));
         else ED_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T) + kPad));
         alloc_ms() += now_ms_host() - t0;
@@ -180,33 +179,13 @@ struct BsrStruct {
     // dataflow schedule: items of <= rows_per_item rows, never straddling a level
     int rows_per_item = 0, nitems = 0;
     DevArray<int> item_row;   // [nitems+1]
-    DevArray<int> item_level; // [nitems]
-    DevArray<int> lev_items;  // [nlev] items per level
-    DevArray<unsigned int> sync; // [nlev + 2]: per-level done counters, ticket
+    DevArray<unsigned int> sync; // [0]: the tagged sweep's ticket counter
     // tagged dataflow sweep (k_sgs_tag): z entries published as {lo32, epoch}{hi32, epoch} words
     mutable DevArray<ulonglong2> ztag; // [nbr * Rb], allocated zeroed at the first sweep
     mutable unsigned int tag_epoch = 0; // last epoch used (one per half sweep)
-    bool sym_pattern = false;           // structurally symmetric (the tagged sweep's precondition)
     bool chain = false;          // narrow levels: single-CTA sweep with CTA barriers
     int avg_rows_per_level = 0;
     DevArray<int> d_lev_ptr;     // device copy of lev_ptr
-    // cluster push sweep (kernels_ring.cu): rows of each level dealt to
-    // ring_cs CTAs, which own their z; CTA c computes, for every row of a
-    // level, the partial row sum over the columns it owns and pushes it to the
-    // row's owner (st.async + mbarrier); the matrix streams through a TMA-fed
-    // ring of per-(level, CTA) chunks
-    int ring_cs = 0;
-    int ring_slice = 0;     // max scalars of z owned by one CTA
-    int ring_cap = 0;       // ring bytes per CTA
-    int ring_part = 0;      // bytes of one partial-sum slot (kRingSlots slots, by level)
-    int64_t ring_npk = 0;   // packed off-diagonal blocks
-    int ring_maxm = 0;      // rows of the widest level (early-sum buffers)
-    DevArray<int4> rchunk;  // [nlev*cs][2] {seg0, rows of the level, pk0, pk1}, {s0, own rows, z offset, barrier flags}
-    DevArray<int4> rseg;    // [nlev*cs*rows] {pk0, pk1, owner << 24 | byte offset in its slot, na << 16 | nb}
-    DevArray<int> rpcol;    // [npk] local z index (scalars) of each packed block's column
-    DevArray<int> rpsrc;    // [npk] stored block index of each packed block
-    DevArray<int> rown;     // [nbr] original rows in (CTA, local) order
-    DevArray<int> rown_ptr; // [cs+1]
     // level-group sweep (kernels_group.cu): consecutive narrow levels merged
     // into groups whose in-group lower triangle is inverted per value change
     int ngrp = 0;                 // 0: no group schedule
@@ -265,7 +244,6 @@ void spmv44(const CoupledOp& K, const double* x, double* y, int nv, int np, cuda
 // Where each block of a pattern (block-CSR order) lands in the stored order.
 struct BsrLayout {
     std::vector<int> perm, inv, lev_ptr;
-    int ring_cs = 0; // > 0: rows of each level are dealt round-robin to ring_cs CTAs, CTA-major (ring_order)
     std::vector<int64_t> addr; // stored block index per pattern block
 };
 
@@ -281,12 +259,8 @@ std::vector<double> bsr_pack_values(const BsrStruct& st, const BsrLayout& lay, c
 // level[i] = 1 + max(level[j] : j < i, (i,j) in pattern).
 void gs_level_order(const BlockPattern& pat, std::vector<int>& order, std::vector<int>& level_of_pos,
                     int& nlev);
-// Cluster push sweep eligibility (kernels_ring.cu): when the operator's
-// vector slices fit a 16-CTA cluster's shared memory and every (level, CTA)
-// chunk fits the TMA ring, reorder the rows inside each level CTA-major
-// (round-robin deal) and return the cluster size; else 0 (order unchanged).
-int ring_order(const BlockPattern& pat, int B, std::vector<int>& order, const std::vector<int>& level_of_pos,
-               int nlev);
+// structural symmetry of a square pattern with sorted columns: required of every Gauss-Seidel
+// operator (a row's later neighbours must wait on it: level schedule and tagged sweep)
 bool pattern_symmetric(const BlockPattern& pat);
 // lanes per block row of the BSR kernels for an average row length (bsr_host.cpp)
 int auto_lanes(double avg_blocks, int entries);
@@ -320,17 +294,6 @@ void sgs_group(const Bsr& A, const double* b, double* z, const double* invd, boo
 void group_prepare(const Bsr& A, const double* invd, DevArray<double>& X, cudaStream_t s);
 // group schedule of a leveled square operator (bsr_host.cpp)
 void group_build(BsrStruct& S, cudaStream_t s);
-// cluster push half sweep (kernels_ring.cu), A.st->ring_cs > 0; packed = ring_pack output
-void sgs_ring(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s,
-              const double* packed);
-// packed off-diagonal blocks + diagonal blocks in stored row order (values as of the call)
-void ring_pack(const Bsr& A, DevArray<double>& packed, cudaStream_t s);
-// push-sweep scratch: double-buffered early sums per segment of a level
-int push_scratch_bytes(int maxm, int B);
-// ring capacity (bytes per CTA) for own slices of `slice` scalars and `parts` bytes of partial slots
-int ring_capacity(int slice, int parts);
-// cluster size the ring sweep runs with on this device (16, 8; 0: unavailable)
-int ring_cluster_size();
 // Jacobi relaxation z += w * inv_diag * (b - t)
 void jacobi_update(double* z, const double* b, const double* t, const double* inv_diag, double w,
                    int64_t n, cudaStream_t s);

@@ -7,10 +7,11 @@
 // exact sequential semantics (amg.cpp:311-322): rows are level-scheduled (a
 // row only reads new values of rows on earlier levels), and inside a 3x3
 // diagonal block the three scalar rows are solved in sweep order by the
-// group leader.  A whole half sweep is ONE persistent dataflow kernel: CTAs
-// take work items in level order from a ticket counter, prefetch their rows'
-// matrix data, wait on the previous level's completion counter, and publish
-// their own, so there is no launch (and no grid-wide barrier) per level.
+// group leader.  A whole half sweep is ONE persistent dataflow kernel
+// (k_sgs_tag): warps take work items in level order from a ticket counter,
+// prefetch their rows' matrix data, and wait only on the tagged values of the
+// neighbours that precede each row, so there is no launch, no grid-wide
+// barrier and no level counter per dependency level.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -142,33 +143,6 @@ __global__ void __launch_bounds__(kThreads) k_spmv2(BsrArgs m1, BsrArgs m2, cons
     }
 }
 
-__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p)
-{
-    unsigned int v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// polling load without the acquire's L1 invalidation (one acquire follows the wait)
-__device__ __forceinline__ unsigned int ld_relaxed(const unsigned int* p)
-{
-    unsigned int v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ unsigned long long globaltimer()
-{
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-
-__device__ __forceinline__ void red_release_add(unsigned int* p, unsigned int v)
-{
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 // Row work of one Gauss-Seidel update (amg.cpp:311-322) for stored row s
 // by a group of L lanes.  Everything that does not depend on z (the lane's
 // first PF blocks, b, inv_diag, the diagonal block, the row's own old z) is
@@ -283,51 +257,6 @@ __device__ __forceinline__ void finish_row(const BsrArgs& m, double* z, bool val
         for (int d = 0; d < B; ++d) z[static_cast<int64_t>(P.row) * B + d] = zs[d];
     }
 }
-
-// One Gauss-Seidel half sweep over wide levels: persistent dataflow kernel.
-template <int B, int L, bool FWD>
-__global__ void __launch_bounds__(kThreads, 2) k_sgs_flow(BsrArgs m, const double* __restrict__ bvec, double* z,
-                                                       const double* __restrict__ invd, int nitems, int nlev,
-                                                       const int* __restrict__ item_row,
-                                                       const int* __restrict__ item_level,
-                                                       const int* __restrict__ lev_items, unsigned int* sync)
-{
-    // enough blocks per lane prefetched that no column index is loaded after the wait
-    constexpr int PF = (B == 3) ? 3 : 4;
-    __shared__ int s_ticket;
-    unsigned int* done = sync;
-    unsigned int* ticket = sync + nlev;
-    const int g = threadIdx.x / L;
-    const int lane = threadIdx.x % L;
-    for (;;) {
-        if (threadIdx.x == 0) s_ticket = static_cast<int>(atomicAdd(ticket, 1u));
-        __syncthreads();
-        const int t = s_ticket;
-        __syncthreads();
-        if (t >= nitems) return;
-        const int item = FWD ? t : nitems - 1 - t;
-        const int lev = item_level[item];
-        const int s = item_row[item] + g;
-        const bool valid = s < item_row[item + 1];
-        RowPref<B, PF> P;
-        prefetch_row<B, L, PF>(m, bvec, invd, z, s, valid, lane, P);
-        const int prev = FWD ? lev - 1 : lev + 1;
-        if (prev >= 0 && prev < nlev) {
-            if (threadIdx.x == 0) {
-                const unsigned int need = static_cast<unsigned int>(lev_items[prev]);
-                // acquire on every poll: the satisfying poll is the acquire (one L2
-                // round trip less on the level's critical path than relaxed polling
-                // followed by a separate acquire load)
-                while (ld_acquire(done + prev) < need) __nanosleep(20);
-            }
-            __syncthreads();
-        }
-        finish_row<B, L, PF, FWD, true>(m, z, valid, lane, P);
-        __syncthreads();
-        if (threadIdx.x == 0) red_release_add(done + lev, 1u); // publishes the CTA's z writes (bar.sync + release)
-    }
-}
-
 
 // ---- tagged dataflow sweep ------------------------------------------------
 // A z entry is published as two 8-byte words {low half, epoch} {high half,
@@ -636,10 +565,6 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
         sgs_group(A, b, z, invd, fwd, s, dense);
         return;
     }
-    if (S.ring_cs > 0) {
-        sgs_ring(A, b, z, invd, fwd, s, dense);
-        return;
-    }
     if (S.chain) {
         ED_LANES(S.Ls, {
             if (fwd)
@@ -650,9 +575,9 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
         after_launch("k_sgs_chain");
         return;
     }
-    // structurally symmetric operators: the tagged dataflow sweep (ED_FLOW_LEGACY=1: level counters)
-    static const bool tagged = std::getenv("ED_FLOW_LEGACY") == nullptr;
-    if (tagged && S.sym_pattern) {
+    // the tagged dataflow sweep (every leveled operator is structurally symmetric: pattern_symmetric
+    // is checked where the level schedule is built)
+    {
         if (S.ztag.n != static_cast<size_t>(S.nbr) * B) {
             S.ztag.alloc(static_cast<size_t>(S.nbr) * B);
             S.ztag.zero(s);
@@ -678,19 +603,7 @@ void launch_sgs(const Bsr& A, const double* b, double* z, const double* invd, bo
                                                                   S.item_row.p, S.sync.p);
         })
         after_launch("k_sgs_tag");
-        return;
     }
-    ED_CUDA(cudaMemsetAsync(S.sync.p, 0, S.sync.n * sizeof(unsigned int), s));
-    const int grid = std::min(S.nitems, 148 * 2);
-    ED_LANES(S.Ls, {
-        if (fwd)
-            k_sgs_flow<B, LL, true><<<grid, kThreads, 0, s>>>(a, b, z, invd, S.nitems, nlev, S.item_row.p,
-                                                             S.item_level.p, S.lev_items.p, S.sync.p);
-        else
-            k_sgs_flow<B, LL, false><<<grid, kThreads, 0, s>>>(a, b, z, invd, S.nitems, nlev, S.item_row.p,
-                                                              S.item_level.p, S.lev_items.p, S.sync.p);
-    })
-    after_launch("k_sgs_flow");
 }
 
 } // namespace
@@ -730,8 +643,7 @@ void sgs_sweep(const Bsr& A, const double* b, double* z, const double* invd, boo
     // pointers, b and inv_diag read, z read and written
     const double bytes = static_cast<double>(S.nnzb) * (8.0 * B * B + 4.0) + 4.0 * (S.nbr + 1) +
                          4.0 * 8.0 * S.nbr * B;
- const char* kname = group_sweep_on(S) ? "k_group_sweep" : S.ring_cs > 0 ? "k_sgs_push" : S.chain ? "k_sgs_chain"
-                                                                                              : "k_sgs_flow";
+    const char* kname = group_sweep_on(S) ? "k_group_sweep" : S.chain ? "k_sgs_chain" : "k_sgs_tag";
     AcctScope acct(s, kname, bytes);
     if (B == 1) return launch_sgs<1>(A, b, z, invd, forward, s, dense);
     if (B == 3) return launch_sgs<3>(A, b, z, invd, forward, s, dense);
@@ -757,7 +669,6 @@ bool group_sweep_on(const BsrStruct& S)
 void sweep_prepare(const Bsr& A, const double* invd, DevArray<double>& aux, cudaStream_t s)
 {
     if (group_sweep_on(*A.st)) return group_prepare(A, invd, aux, s);
-    if (A.st->ring_cs > 0) return ring_pack(A, aux, s); // push sweep: packed blocks (kernels_ring.cu)
     aux.release();
 }
 

@@ -18,9 +18,7 @@ void BlockSys::build_structure(cudaStream_t s)
     std::vector<int> order, lvl;
     int nlev = 0;
     gs_level_order(pA, order, lvl, nlev);
-    const int rcs = ring_order(pA, Bv, order, lvl, nlev);
     lA = make_layout(pA, order, lvl);
-    lA.ring_cs = rcs;
     lB = make_layout(pB, order, lvl); // same slicing as A
     std::vector<int> porder(pD.nbr);
     std::iota(porder.begin(), porder.end(), 0);
@@ -114,9 +112,7 @@ void BlockSys::build_shat_symbolic(cudaStream_t s)
     std::vector<int> order, lvl;
     int nlev = 0;
     gs_level_order(pS, order, lvl, nlev);
-    const int rcs = ring_order(pS, 1, order, lvl, nlev);
     BsrLayout lS = make_layout(pS, order, lvl);
-    lS.ring_cs = rcs;
     sS = bsr_make_struct(pS, lS, 1, 1, s);
     cb_off.upload(hcb_off, s);
     d_off.upload(hd_off, s);

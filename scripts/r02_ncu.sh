@@ -10,8 +10,8 @@ echo "launch rc=$?" > gpurun_out/ncu_rc.txt
 timeout 900 $NCU --set full --import-source on --clock-control none -k regex:k_group_sweep -s 30 -c 1 \
   -o gpurun_out/r02_group_sweep python scripts/acct40.py > gpurun_out/ncu_group.log 2>&1
 echo "group rc=$?" >> gpurun_out/ncu_rc.txt
-timeout 900 $NCU --set full --import-source on --clock-control none -k regex:k_sgs_flow -s 30 -c 1 \
-  -o gpurun_out/r02_flow python scripts/acct40.py > gpurun_out/ncu_flow.log 2>&1
+timeout 900 $NCU --set full --import-source on --clock-control none -k regex:k_sgs_tag -s 30 -c 1 \
+  -o gpurun_out/r02_tag python scripts/acct40.py > gpurun_out/ncu_flow.log 2>&1
 echo "flow rc=$?" >> gpurun_out/ncu_rc.txt
 timeout 900 $NCU --metrics sm__sass_thread_inst_executed_op_dadd_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum,sm__sass_thread_inst_executed_op_dfma_pred_on.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
   --clock-control none -k regex:"k_tangent|k_residual|k_k4_split|k_traction" -c 8 --csv --log-file gpurun_out/r02_asm_flops.csv \

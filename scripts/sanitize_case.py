@@ -1,6 +1,6 @@
 """One first Newton corrector pass on a small seeded cube (compute-sanitizer target):
 every kernel family of the path runs -- element kernels, K4 split, coupled SpMV,
-dataflow / push / group / chain sweeps, dense tail, Krylov vector kernels."""
+tagged dataflow / group / chain sweeps, dense tail, Krylov vector kernels."""
 import os
 import sys
 
