@@ -201,16 +201,10 @@ void group_build(BsrStruct& S, cudaStream_t s)
     }
     S.grp_tinv = tot;
     S.grp_maxm = maxm;
-    // cluster scope (one 16-CTA cluster: ~0.1 us barriers, but 16 SMs of
-    // bandwidth) measured slower than the whole grid at 40^3 for every level
-    // (profiles/r02/sweeps.md); opt-in below ED_GROUP_CLUSTER_MB
-    static const double cl_max = std::getenv("ED_GROUP_CLUSTER_MB") ? std::atof(std::getenv("ED_GROUP_CLUSTER_MB")) : 0.0;
-    const double sweep_bytes = static_cast<double>(S.nnzb) * (8.0 * B * B + 4.0) + 8.0 * static_cast<double>(tot);
-    S.grp_cluster = sweep_bytes <= cl_max * 1e6;
     // measured at 40^3 (profiles/r02/sweeps.md): one grid barrier costs ~1.3 us,
     // so level groups pay on narrow deep schedules (a coarse level: ~36 block
     // rows per level -> 9 levels per group step); wide levels stay on the
-    // dataflow / cluster push sweeps, which need no grid-wide barrier per level
+    // tagged dataflow sweep, which needs no grid-wide barrier per level
     static const int max_rpl = std::getenv("ED_GROUP_MAX_RPL") ? std::atoi(std::getenv("ED_GROUP_MAX_RPL")) : 64;
     S.grp_use = nlev > 0 && static_cast<double>(n) / nlev <= max_rpl && tot > 0;
     S.ntchunk = static_cast<int>(chunks.size());

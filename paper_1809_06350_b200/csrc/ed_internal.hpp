@@ -192,7 +192,6 @@ struct BsrStruct {
     int grp_maxm = 0;             // scalar rows of the largest multi-level group
     int64_t grp_tinv = 0;         // packed T^-1 doubles per direction (0: all groups single-level)
     int ntchunk = 0;              // (group, 32-column) chunks of the T^-1 build
-    bool grp_cluster = false;     // sweep inside one 16-CTA cluster (cheap barriers) instead of the whole grid
     bool grp_use = false;         // the group sweep is this operator's sweep (narrow, deep schedules)
     DevArray<int4> grp;           // [ngrp] {r0, r1, m (0: single level), 0} stored rows
     DevArray<long long> grp_toff; // [ngrp] offset of the group's packed T^-1

@@ -36,7 +36,6 @@ namespace {
 
 constexpr int kGT = 256; // threads per CTA of the sweep kernel
 constexpr int kGroupMaxRows = 1024;
-constexpr int kGroupCluster = 16; // CTAs of the cluster-scoped sweep (non-portable size) // scalar rows of a multi-level group (T^-1 row prefetch depth)
 
 struct GrpArgs {
     const int* rowptr;
@@ -68,25 +67,14 @@ __device__ __forceinline__ void g_red_release(unsigned int* p, unsigned int v)
 // Grid barrier over all (co-resident) CTAs, split in two so that loads of the
 // next step's z-independent data can be issued between arrive and wait (a
 // release would otherwise wait for them).  `target` counts arrivals so far.
-template <bool CL>
 __device__ __forceinline__ void bar_arrive(unsigned int* ctr)
 {
-    if (CL) {
-        // cluster scope: the hardware barrier (release orders this thread's z / s stores)
-        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-        return;
-    }
     __syncthreads();
     if (threadIdx.x == 0) g_red_release(ctr, 1u);
 }
 
-template <bool CL>
 __device__ __forceinline__ void bar_wait(unsigned int* ctr, unsigned int& target)
 {
-    if (CL) {
-        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-        return;
-    }
     target += gridDim.x;
     if (threadIdx.x == 0) {
         // bounded spin: a grid whose CTAs are not all resident would wait
@@ -251,7 +239,7 @@ __device__ __forceinline__ void grow_finish(const GrpArgs& a, double* z, double*
 // dealt round-robin over the CTAs first (lane group lg of CTA b takes row
 // b + lg * grid), so a level's rows spread over the whole GPU; trip counts
 // are CTA-uniform, so every lane reaches the shuffles.
-template <int B, int L, bool FWD, bool CL>
+template <int B, int L, bool FWD>
 __global__ void __launch_bounds__(kGT, 1) k_group_sweep(GrpArgs a, const double* __restrict__ bvec, double* z,
                                                      const double* __restrict__ invd, const double* __restrict__ X,
                                                      double* sbuf, unsigned int* bar)
@@ -287,7 +275,7 @@ __global__ void __launch_bounds__(kGT, 1) k_group_sweep(GrpArgs a, const double*
                 if (q0 > 0) grow_load<B, L, PF>(a, bvec, invd, z, sr_of(r0, r1, q), q < nr, lane, P);
                 grow_finish<B, L, PF, FWD, true>(a, z, sbuf, sr_of(r0, r1, q), r0, r1, lane, P);
             }
-            bar_arrive<CL>(bar);
+            bar_arrive(bar);
             // this warp's first phase-B row of T^-1 into registers during the barrier
             const double* Xg = X + a.toff[g];
             const int i0 = blockIdx.x + warp * gridDim.x;
@@ -298,7 +286,7 @@ __global__ void __launch_bounds__(kGT, 1) k_group_sweep(GrpArgs a, const double*
                 const int j = wl + 32 * q;
                 xv[q] = (i0 < m && j <= i0) ? __ldg(xr0 + j) : 0.0;
             }
-            bar_wait<CL>(bar, target);
+            bar_wait(bar, target);
             // phase B: z_G = T^-1 s_G, one warp per scalar row of the group
             for (int i = i0; i < m; i += (kGT / 32) * gridDim.x) {
                 const double* xr = Xg + static_cast<int64_t>(i) * (i + 1) / 2;
@@ -324,14 +312,14 @@ __global__ void __launch_bounds__(kGT, 1) k_group_sweep(GrpArgs a, const double*
                 }
             }
         }
-        bar_arrive<CL>(bar);
+        bar_arrive(bar);
         // the next group's rows: everything z-independent, during the barrier
         if (t + 1 < a.ngrp) {
             const int4 gn = a.grp[FWD ? t + 1 : a.ngrp - 2 - t];
             const int q = blockIdx.x + lg * gridDim.x;
             grow_load<B, L, PF>(a, bvec, invd, z, sr_of(gn.x, gn.y, q), q < gn.y - gn.x, lane, P);
         }
-        bar_wait<CL>(bar, target);
+        bar_wait(bar, target);
     }
 }
 
@@ -418,7 +406,7 @@ int sweep_grid()
     if (!g) {
         int sms = 0, occ = 0;
         ED_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        ED_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group_sweep<3, 32, true, false>, kGT, 0));
+        ED_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group_sweep<3, 32, true>, kGT, 0));
         static const int per_sm = std::getenv("ED_SWEEP_CTAS") ? std::atoi(std::getenv("ED_SWEEP_CTAS")) : 1;
         g = sms * std::max(1, std::min(occ, per_sm));
         // ED_SWEEP_GRID=n: fewer CTAs (cheaper barrier, less bandwidth)
@@ -436,52 +424,21 @@ int sweep_grid()
     default: { constexpr int LL = 32; __VA_ARGS__; break; } \
     }
 
-template <int B, int LL, bool FWD>
-void launch_one(const GrpArgs& a, const double* b, double* z, const double* invd, const double* X, double* sbuf,
-                unsigned int* bar, bool cluster, cudaStream_t s)
-{
-    if (!cluster) {
-        k_group_sweep<B, LL, FWD, false><<<sweep_grid(), kGT, 0, s>>>(a, b, z, invd, X, sbuf, bar);
-        return;
-    }
-    auto kern = k_group_sweep<B, LL, FWD, true>;
-    static bool attr_done[64] = {};
-    int dev = 0;
-    ED_CUDA(cudaGetDevice(&dev));
-    if (!attr_done[dev & 63]) {
-        ED_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr_done[dev & 63] = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kGroupCluster, 1, 1);
-    cfg.blockDim = dim3(kGT, 1, 1);
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = kGroupCluster;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    ED_CUDA(cudaLaunchKernelEx(&cfg, kern, a, b, z, invd, X, sbuf, bar));
-}
-
 template <int B>
 void launch_group(const Bsr& A, const double* b, double* z, const double* invd, bool fwd, cudaStream_t s,
                   const double* X)
 {
     const BsrStruct& S = *A.st;
     const GrpArgs a = gargs_of(A);
-    const bool cluster = S.grp_cluster;
-    if (!cluster) ED_CUDA(cudaMemsetAsync(S.gbar.p, 0, sizeof(unsigned int), s));
+    ED_CUDA(cudaMemsetAsync(S.gbar.p, 0, sizeof(unsigned int), s));
     const double* Xd = X ? X + (fwd ? 0 : S.grp_tinv) : nullptr;
     ED_GLANES(S.Ls, {
         if (fwd)
-            launch_one<B, LL, true>(a, b, z, invd, Xd, S.gsbuf.p, S.gbar.p, cluster, s);
+            k_group_sweep<B, LL, true><<<sweep_grid(), kGT, 0, s>>>(a, b, z, invd, Xd, S.gsbuf.p, S.gbar.p);
         else
-            launch_one<B, LL, false>(a, b, z, invd, Xd, S.gsbuf.p, S.gbar.p, cluster, s);
+            k_group_sweep<B, LL, false><<<sweep_grid(), kGT, 0, s>>>(a, b, z, invd, Xd, S.gsbuf.p, S.gbar.p);
     })
-    after_launch(cluster ? "k_group_sweep(cluster)" : "k_group_sweep");
+    after_launch("k_group_sweep");
 }
 
 } // namespace
