@@ -221,8 +221,7 @@ void group_build(BsrStruct& S, cudaStream_t s)
             const int sc = identity ? c : S.h_inv[c];
             if (c == row) code[k] = 3;
             else if (grp_of[sr] >= 0 && grp_of[sc] == grp_of[sr]) code[k] = sc < sr ? 1 : 2;
-            else if (sc < sr) code[k] = 4; // another group, earlier in stored order (swept before in a forward sweep)
-            if (grp_of[sr] >= 0 && code[k] != 0 && code[k] != 4) ++cnt;
+            if (grp_of[sr] >= 0 && code[k] != 0) ++cnt;
         }
         gcnt[sr] = cnt;
     }
@@ -233,7 +232,7 @@ void group_build(BsrStruct& S, cudaStream_t s)
         if (grp_of[sr] < 0) continue;
         int o = gptr[sr];
         for (int k = S.h_rowptr[sr]; k < S.h_rowptr[sr + 1]; ++k)
-            if (code[k] != 0 && code[k] != 4) gblk[o++] = k;
+            if (code[k] != 0) gblk[o++] = k;
     }
     S.grp.upload(grp, s);
     S.grp_toff.upload(toff, s);

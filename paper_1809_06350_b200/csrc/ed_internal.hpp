@@ -182,7 +182,6 @@ struct BsrStruct {
     DevArray<unsigned int> sync; // [0]: the tagged sweep's ticket counter
     // tagged dataflow sweep (k_sgs_tag): z entries published as {lo32, epoch}{hi32, epoch} words
     mutable DevArray<ulonglong2> ztag; // [nbr * Rb], allocated zeroed at the first sweep
-    mutable DevArray<ulonglong2> stag; // [nbr * Rb] tagged phase-A sums of the tagged group sweep (stored order)
     mutable unsigned int tag_epoch = 0; // last epoch used (one per half sweep)
     bool chain = false;          // narrow levels: single-CTA sweep with CTA barriers
     int avg_rows_per_level = 0;
@@ -196,7 +195,7 @@ struct BsrStruct {
     bool grp_use = false;         // the group sweep is this operator's sweep (narrow, deep schedules)
     DevArray<int4> grp;           // [ngrp] {r0, r1, m (0: single level), 0} stored rows
     DevArray<long long> grp_toff; // [ngrp] offset of the group's packed T^-1
-    DevArray<unsigned char> bcode; // [nnzb] 0 / 4 other group later / earlier in stored order, 1 in-group lower, 2 in-group upper, 3 diagonal
+    DevArray<unsigned char> bcode; // [nnzb] 0 other group, 1 in-group lower, 2 in-group upper, 3 diagonal
     DevArray<int> gptr, gblk;     // in-group blocks per stored row (multi-level groups)
     DevArray<int2> tchunk;        // [ntchunk] {group, j0}
     DevArray<unsigned int> gbar;  // grid-barrier counter

@@ -26,7 +26,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdio>
 #include <cstdlib>
 
 #include "ed_internal.hpp"
@@ -47,7 +46,7 @@ struct GrpArgs {
     const double* val;
     const int4* grp;              // {r0, r1, m (0: single level), pad}
     const long long* toff;        // packed T^-1 offset of each group (doubles)
-    const unsigned char* bcode;   // per block: 0 / 4 other group (later / earlier in stored order), 1 in-group lower, 2 in-group upper, 3 diagonal
+    const unsigned char* bcode;   // per block: 0 other group, 1 in-group lower, 2 in-group upper, 3 diagonal
     const int* gptr;              // [nbr+1] in-group blocks of each stored row (multi-level groups)
     const int* gblk;
     int ngrp;
@@ -117,33 +116,15 @@ struct GRow {
     double b[B], id[B], D[B * B], zs[B];
 };
 
-// The row's indices (one dependent load level) ...
-struct GIdx {
-    int row, kb, ke, dp;
-    bool valid;
-};
-
-__device__ __forceinline__ GIdx grow_index(const GrpArgs& a, int sr, bool valid, int lane)
-{
-    GIdx I;
-    I.valid = valid;
-    I.row = valid ? (a.perm ? __ldg(a.perm + sr) : sr) : 0;
-    I.kb = valid ? __ldg(a.rowptr + sr) + lane : 0;
-    I.ke = valid ? __ldg(a.rowptr + sr + 1) : 0;
-    I.dp = valid && lane == 0 ? __ldg(a.dpos + sr) : -1;
-    return I;
-}
-
-// ... and everything they address (the second level).
 template <int B, int L, int PF>
-__device__ __forceinline__ void grow_data(const GrpArgs& a, const double* __restrict__ bvec,
-                                          const double* __restrict__ invd, const double* z, const GIdx& I, int lane,
-                                          GRow<B, PF>& P)
+__device__ __forceinline__ void grow_load(const GrpArgs& a, const double* __restrict__ bvec,
+                                          const double* __restrict__ invd, const double* z, int sr, bool valid,
+                                          int lane, GRow<B, PF>& P)
 {
-    P.valid = I.valid;
-    P.row = I.row;
-    P.kb = I.kb;
-    P.ke = I.ke;
+    P.valid = valid;
+    P.row = valid ? (a.perm ? a.perm[sr] : sr) : 0;
+    P.kb = valid ? a.rowptr[sr] + lane : 0;
+    P.ke = valid ? a.rowptr[sr + 1] : 0;
 #pragma unroll
     for (int q = 0; q < PF; ++q) {
         const int k = P.kb + q * L;
@@ -153,8 +134,8 @@ __device__ __forceinline__ void grow_data(const GrpArgs& a, const double* __rest
 #pragma unroll
         for (int e = 0; e < B * B; ++e) P.v[q][e] = in ? __ldg(a.val + static_cast<int64_t>(k) * (B * B) + e) : 0.0;
     }
-    if (I.valid && lane == 0) {
-        const int dp = I.dp;
+    if (valid && lane == 0) {
+        const int dp = a.dpos[sr];
 #pragma unroll
         for (int d = 0; d < B; ++d) {
             const int64_t i = static_cast<int64_t>(P.row) * B + d;
@@ -167,21 +148,13 @@ __device__ __forceinline__ void grow_data(const GrpArgs& a, const double* __rest
     }
 }
 
-template <int B, int L, int PF>
-__device__ __forceinline__ void grow_load(const GrpArgs& a, const double* __restrict__ bvec,
-                                          const double* __restrict__ invd, const double* z, int sr, bool valid,
-                                          int lane, GRow<B, PF>& P)
-{
-    grow_data<B, L, PF>(a, bvec, invd, z, grow_index(a, sr, valid, lane), lane, P);
-}
-
 // does the block's scalar (r, d) enter the sum (everything not in T_G)?
 template <bool FWD, bool MULTI>
 __device__ __forceinline__ bool takes(int code, int r, int d)
 {
     if (!MULTI) return code != 3;                         // single level: all off-diagonal blocks
     if (code == 3) return FWD ? d > r : d < r;             // diagonal block: the far side of the sweep
-    return code == 0 || code == 4 || code == (FWD ? 2 : 1); // other groups; in-group blocks not yet swept
+    return code == 0 || code == (FWD ? 2 : 1);             // other groups; in-group blocks not yet swept
 }
 
 // Row sums over the z-dependent part.  MULTI = false: the full Gauss-Seidel
@@ -350,309 +323,6 @@ __global__ void __launch_bounds__(kGT, 1) k_group_sweep(GrpArgs a, const double*
     }
 }
 
-// ---- tagged level-group sweep ---------------------------------------------
-// The same group steps without grid barriers: s_G and z are published as
-// {low half, epoch} {high half, epoch} words (kernels_sparse.cu, k_sgs_tag: an
-// 8-byte word whose tag equals this half sweep's epoch carries this half
-// sweep's value), phase-A rows poll only the z of blocks whose column lies in a
-// group swept EARLIER, phase-B rows poll the s_j (j <= i) of their own group.
-// Old values (later groups, the not-yet-swept side of the own group) come from
-// the plain z: their owners overwrite them only after consuming, directly or
-// through s, a tagged value this row publishes after its reads (symmetric
-// pattern).  Every wait is on work of an earlier phase of the same or an
-// earlier group, and every CTA walks the groups in order, so the persistent
-// grid cannot deadlock; waits are bounded (trap) all the same.
-__device__ __forceinline__ void g_st_tagged(ulonglong2* p, double v, unsigned int tag)
-{
-    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
-    const unsigned long long t = static_cast<unsigned long long>(tag) << 32;
-    const unsigned long long w0 = (b & 0xffffffffull) | t, w1 = (b >> 32) | t;
-    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
-}
-
-__device__ __forceinline__ bool g_ld_tagged(const ulonglong2* p, unsigned int tag, double& v)
-{
-    unsigned long long w0, w1;
-    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
-    v = __longlong_as_double(static_cast<long long>((w0 & 0xffffffffull) | (w1 << 32)));
-    return static_cast<unsigned int>(w0 >> 32) == tag && static_cast<unsigned int>(w1 >> 32) == tag;
-}
-
-// a stuck wait traps after ~5 s instead of hanging the device
-struct SpinGuard {
-    long long t0 = 0;
-    __device__ __forceinline__ void tick()
-    {
-        if (t0 == 0) t0 = clock64();
-        else if (clock64() - t0 > 10000000000LL) __trap();
-    }
-};
-
-// a block of another group whose column is swept before this row's group: code 4 (earlier in stored
-// order) in a forward sweep, code 0 (later) in a backward sweep
-template <bool FWD>
-__device__ __forceinline__ bool swept_before(int code)
-{
-    return code == (FWD ? 4 : 0);
-}
-
-// z of NQ blocks per lane: blocks of earlier groups (fresh[q]) polled in the tagged copy, the rest
-// from the plain z.  Warp-uniform loop.
-template <int B, int NQ>
-__device__ __forceinline__ void g_gather(const int (&c)[NQ], const bool (&fresh)[NQ], const double* z,
-                                         const ulonglong2* zt, unsigned int epoch, double (&zv)[NQ][B])
-{
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        const int64_t cc = c[q] >= 0 ? c[q] : 0;
-#pragma unroll
-        for (int d = 0; d < B; ++d) zv[q][d] = fresh[q] ? 0.0 : __ldcg(z + cc * B + d);
-    }
-    SpinGuard guard;
-    for (;;) {
-        bool ok = true;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            if (!fresh[q]) continue;
-#pragma unroll
-            for (int d = 0; d < B; ++d) ok = g_ld_tagged(zt + static_cast<int64_t>(c[q]) * B + d, epoch, zv[q][d]) && ok;
-        }
-        if (__all_sync(0xffffffffu, ok)) break;
-        guard.tick();
-    }
-}
-
-template <int B, int PF>
-struct GFresh {
-    bool f[PF];
-};
-
-// Row sums of grow_finish with tagged gathers.  MULTI = false: the row's full update, z published
-// tagged and plain.  MULTI = true: s_i published tagged at spos0 + local index.
-template <int B, int L, int PF, bool FWD, bool MULTI>
-__device__ __forceinline__ void grow_finish_tagged(const GrpArgs& a, double* z, ulonglong2* zt, ulonglong2* st,
-                                                   unsigned int epoch, int sr, int r0, int r1, int lane,
-                                                   const GRow<B, PF>& P, const GFresh<B, PF>& F)
-{
-    double acc[B];
-#pragma unroll
-    for (int r = 0; r < B; ++r) acc[r] = 0.0;
-    {
-        double zv[PF][B];
-        g_gather<B, PF>(P.c, F.f, z, zt, epoch, zv);
-#pragma unroll
-        for (int q = 0; q < PF; ++q) {
-            if (P.c[q] < 0) continue;
-#pragma unroll
-            for (int d = 0; d < B; ++d)
-#pragma unroll
-                for (int r = 0; r < B; ++r)
-                    if (takes<FWD, MULTI>(P.code[q], r, d)) acc[r] = fma(P.v[q][r * B + d], zv[q][d], acc[r]);
-        }
-    }
-    constexpr int NB = B == 3 ? 4 : 8;
-    int more = 0;
-    for (int k0 = P.kb + PF * L; k0 < P.ke; k0 += NB * L) ++more;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) more = max(more, __shfl_xor_sync(0xffffffffu, more, o));
-    for (int it = 0; it < more; ++it) {
-        const int k0 = P.kb + (PF + it * NB) * L;
-        int cb[NB], codeb[NB];
-        bool fb[NB];
-        double vb[NB][B * B], zb[NB][B];
-#pragma unroll
-        for (int p = 0; p < NB; ++p) {
-            const int k = k0 + p * L;
-            const bool in = P.valid && k < P.ke;
-            cb[p] = in ? __ldg(a.col + k) : -1;
-            codeb[p] = in ? a.bcode[k] : -1;
-#pragma unroll
-            for (int e = 0; e < B * B; ++e) vb[p][e] = in ? __ldg(a.val + static_cast<int64_t>(k) * (B * B) + e) : 0.0;
-        }
-#pragma unroll
-        for (int p = 0; p < NB; ++p) fb[p] = cb[p] >= 0 && swept_before<FWD>(codeb[p]);
-        g_gather<B, NB>(cb, fb, z, zt, epoch, zb);
-#pragma unroll
-        for (int p = 0; p < NB; ++p)
-#pragma unroll
-            for (int d = 0; d < B; ++d)
-#pragma unroll
-                for (int r = 0; r < B; ++r)
-                    if (codeb[p] >= 0 && takes<FWD, MULTI>(codeb[p], r, d)) acc[r] = fma(vb[p][r * B + d], zb[p][d], acc[r]);
-    }
-#pragma unroll
-    for (int r = 0; r < B; ++r) acc[r] = lane_sum<L>(acc[r]);
-    if (!P.valid || lane != 0) return;
-    if (MULTI) {
-#pragma unroll
-        for (int c = 0; c < B; ++c)
-            g_st_tagged(st + static_cast<int64_t>(r0) * B + local_of<B, FWD>(sr, c, r0, r1), P.b[c] - acc[c], epoch);
-        return;
-    }
-    double zs[B];
-#pragma unroll
-    for (int d = 0; d < B; ++d) zs[d] = P.zs[d];
-#pragma unroll
-    for (int ci = 0; ci < B; ++ci) {
-        const int c = FWD ? ci : B - 1 - ci;
-        double v = P.b[c] - acc[c];
-#pragma unroll
-        for (int d = 0; d < B; ++d)
-            if (d != c) v -= P.D[c * B + d] * zs[d];
-        zs[c] = v * P.id[c];
-    }
-#pragma unroll
-    for (int d = 0; d < B; ++d) g_st_tagged(zt + static_cast<int64_t>(P.row) * B + d, zs[d], epoch);
-#pragma unroll
-    for (int d = 0; d < B; ++d) z[static_cast<int64_t>(P.row) * B + d] = zs[d];
-}
-
-template <int B, int L, int PF, bool FWD>
-__device__ __forceinline__ void grow_data_tagged(const GrpArgs& a, const double* __restrict__ bvec,
-                                                 const double* __restrict__ invd, const double* z, const GIdx& I,
-                                                 int lane, GRow<B, PF>& P, GFresh<B, PF>& F)
-{
-    grow_data<B, L, PF>(a, bvec, invd, z, I, lane, P);
-#pragma unroll
-    for (int q = 0; q < PF; ++q) F.f[q] = P.c[q] >= 0 && swept_before<FWD>(P.code[q]);
-}
-
-template <int B, int L, bool FWD>
-__global__ void __launch_bounds__(kGT, 1) k_group_tag(GrpArgs a, const double* __restrict__ bvec, double* z,
-                                                   const double* __restrict__ invd, const double* __restrict__ X,
-                                                   ulonglong2* zt, ulonglong2* st, unsigned int epoch)
-{
-    constexpr int PF = B == 3 ? 3 : 4;
-    constexpr int XQ = kGroupMaxRows / 32;
-    constexpr int GPC = kGT / L;
-    const int lg = threadIdx.x / L, lane = threadIdx.x % L;
-    const int warp = threadIdx.x / 32, wl = threadIdx.x % 32;
-    const int stride = GPC * gridDim.x;
-    __shared__ double s_sm[2][kGroupMaxRows]; // the group's s, double-buffered by group parity
-    GRow<B, PF> P;
-    GFresh<B, PF> F;
-    auto sr_of = [&](int r0, int r1, int q) { return FWD ? r0 + q : r1 - 1 - q; };
-    auto grp_at = [&](int t) { return t < a.ngrp ? a.grp[FWD ? t : a.ngrp - 1 - t] : make_int4(0, 0, 0, 0); };
-    auto toff_at = [&](int t) { return t < a.ngrp ? a.toff[FWD ? t : a.ngrp - 1 - t] : 0LL; };
-    // this lane group's first row of a group: indices one group step ahead of the data they address,
-    // so no dependent load chain sits between a group's two phases
-    const int qf = blockIdx.x + lg * gridDim.x;
-    auto index_of = [&](const int4& gr) { return grow_index(a, sr_of(gr.x, gr.y, qf), qf < gr.y - gr.x, lane); };
-    int4 gi = grp_at(0), gn = grp_at(1);
-    long long toff_cur = toff_at(0), toff_nxt = toff_at(1);
-    grow_data_tagged<B, L, PF, FWD>(a, bvec, invd, z, index_of(gi), lane, P, F);
-    GIdx In = index_of(gn);
-    for (int t = 0; t < a.ngrp; ++t) {
-        const int r0 = gi.x, r1 = gi.y, m = gi.z;
-        const int nr = r1 - r0;
-        const int4 gnn = grp_at(t + 2); // two steps ahead: arrives during this step
-        const long long toff_nn = toff_at(t + 2);
-        auto load_next = [&]() {
-            if (t + 1 < a.ngrp) grow_data_tagged<B, L, PF, FWD>(a, bvec, invd, z, In, lane, P, F);
-        };
-        auto rotate = [&]() {
-            gi = gn;
-            gn = gnn;
-            toff_cur = toff_nxt;
-            toff_nxt = toff_nn;
-            In = index_of(gn);
-        };
-        if (m == 0) {
-            for (int q0 = 0; q0 < nr; q0 += stride) {
-                const int q = q0 + qf;
-                if (q0 > 0)
-                    grow_data_tagged<B, L, PF, FWD>(a, bvec, invd, z, grow_index(a, sr_of(r0, r1, q), q < nr, lane),
-                                                    lane, P, F);
-                grow_finish_tagged<B, L, PF, FWD, false>(a, z, zt, st, epoch, sr_of(r0, r1, q), r0, r1, lane, P, F);
-            }
-            load_next();
-            rotate();
-            continue;
-        }
-        for (int q0 = 0; q0 < nr; q0 += stride) {
-            const int q = q0 + qf;
-            if (q0 > 0)
-                grow_data_tagged<B, L, PF, FWD>(a, bvec, invd, z, grow_index(a, sr_of(r0, r1, q), q < nr, lane), lane,
-                                                P, F);
-            grow_finish_tagged<B, L, PF, FWD, true>(a, z, zt, st, epoch, sr_of(r0, r1, q), r0, r1, lane, P, F);
-        }
-        // this warp's first phase-B row of T^-1 and the next group's rows: issued before the s polls
-        const double* Xg = X + toff_cur;
-        const ulonglong2* sg = st + static_cast<int64_t>(r0) * B;
-        const int i0 = blockIdx.x + warp * gridDim.x;
-        double xv[XQ];
-        {
-            const double* xr0 = Xg + static_cast<int64_t>(i0) * (i0 + 1) / 2;
-#pragma unroll
-            for (int q = 0; q < XQ; ++q) {
-                const int j = wl + 32 * q;
-                xv[q] = (i0 < m && j <= i0) ? __ldg(xr0 + j) : 0.0;
-            }
-        }
-        load_next();
-        // phase B: z_G = T^-1 s_G, one warp per scalar row of the group.  The CTA polls the group's
-        // s once, cooperatively (thread tid takes j = tid, tid + 256, ...), into shared memory;
-        // every warp polling all s_j itself costs m^2 / 2 tagged loads per round and group.
-        if (static_cast<int>(blockIdx.x) < m) { // CTA-uniform: this CTA has phase-B rows
-            double* sm = s_sm[t & 1];
-            if (m <= kGroupMaxRows) {
-                SpinGuard guard;
-                for (;;) {
-                    bool ok = true;
-                    for (int j = threadIdx.x; j < m; j += kGT) {
-                        double sv;
-                        ok = g_ld_tagged(sg + j, epoch, sv) && ok;
-                        sm[j] = sv;
-                    }
-                    if (__syncthreads_and(ok)) break;
-                    guard.tick();
-                }
-            }
-            for (int i = i0; i < m; i += (kGT / 32) * gridDim.x) {
-                const double* xr = Xg + static_cast<int64_t>(i) * (i + 1) / 2;
-                if (i != i0) {
-#pragma unroll
-                    for (int q = 0; q < XQ; ++q) {
-                        const int j = wl + 32 * q;
-                        xv[q] = j <= i ? __ldg(xr + j) : 0.0;
-                    }
-                }
-                double acc = 0.0;
-                if (m <= kGroupMaxRows) {
-#pragma unroll
-                    for (int q = 0; q < XQ; ++q) {
-                        const int j = wl + 32 * q;
-                        if (j <= i) acc = fma(xv[q], sm[j], acc);
-                    }
-                } else { // groups larger than kGroupMaxRows (ED_GROUP_ROWS): every warp polls its own s_j
-                    SpinGuard guard;
-                    for (;;) {
-                        bool ok = true;
-                        acc = 0.0;
-                        for (int j = wl; j <= i; j += 32) {
-                            double sv;
-                            ok = g_ld_tagged(sg + j, epoch, sv) && ok;
-                            acc = fma(__ldg(xr + j), sv, acc);
-                        }
-                        if (__all_sync(0xffffffffu, ok)) break;
-                        guard.tick();
-                    }
-                }
-                acc = lane_sum<32>(acc);
-                if (wl == 0) {
-                    const int p = i / B, c = i % B;
-                    const int sr = sr_of(r0, r1, p);
-                    const int cc = FWD ? c : B - 1 - c;
-                    const int row = a.perm ? a.perm[sr] : sr;
-                    g_st_tagged(zt + static_cast<int64_t>(row) * B + cc, acc, epoch);
-                    z[static_cast<int64_t>(row) * B + cc] = acc;
-                }
-            }
-        }
-        rotate();
-    }
-}
-
 // T_G^-1 for both directions: one warp per (group, 32 columns [j0, j0+32)),
 // forward substitution over the group's scalar rows in processing order:
 //   x_i = invd_i * (e_ij - sum_{k before i in G} a_ik x_k)
@@ -760,32 +430,8 @@ void launch_group(const Bsr& A, const double* b, double* z, const double* invd, 
 {
     const BsrStruct& S = *A.st;
     const GrpArgs a = gargs_of(A);
-    const double* Xd = X ? X + (fwd ? 0 : S.grp_tinv) : nullptr;
-    static const bool tagged = std::getenv("ED_GROUP_BARRIER") == nullptr;
-    if (tagged) {
-        const size_t nsc = static_cast<size_t>(S.nbr) * B;
-        if (S.ztag.n != nsc || S.stag.n != nsc) {
-            S.ztag.alloc(nsc);
-            S.stag.alloc(nsc);
-            S.ztag.zero(s);
-            S.stag.zero(s);
-            S.tag_epoch = 0;
-        }
-        if (++S.tag_epoch == 0) { // epoch wrap: start over from clean tags
-            S.ztag.zero(s);
-            S.stag.zero(s);
-            S.tag_epoch = 1;
-        }
-        ED_GLANES(S.Ls, {
-            if (fwd)
-                k_group_tag<B, LL, true><<<sweep_grid(), kGT, 0, s>>>(a, b, z, invd, Xd, S.ztag.p, S.stag.p, S.tag_epoch);
-            else
-                k_group_tag<B, LL, false><<<sweep_grid(), kGT, 0, s>>>(a, b, z, invd, Xd, S.ztag.p, S.stag.p, S.tag_epoch);
-        })
-        after_launch("k_group_tag");
-        return;
-    }
     ED_CUDA(cudaMemsetAsync(S.gbar.p, 0, sizeof(unsigned int), s));
+    const double* Xd = X ? X + (fwd ? 0 : S.grp_tinv) : nullptr;
     ED_GLANES(S.Ls, {
         if (fwd)
             k_group_sweep<B, LL, true><<<sweep_grid(), kGT, 0, s>>>(a, b, z, invd, Xd, S.gsbuf.p, S.gbar.p);
