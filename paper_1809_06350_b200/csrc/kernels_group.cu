@@ -357,32 +357,31 @@ __global__ void __launch_bounds__(128) k_group_tinv(GrpArgs a, const double* __r
                 msc = a.inv ? a.inv[c] : c;
             }
             const int nb = min(32, q1 - qb);
-            // eight blocks at a time: all coefficient and X loads of the sub-batch in flight, then
-            // the subtractions in block order (a skipped term enters as 0 * 0, which leaves acc as is)
-            for (int e0 = 0; e0 < nb; e0 += 8) {
-                double cf[8][B], xs[8][B];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int e = e0 + u;
-                    const bool in = e < nb;
-                    const int k = __shfl_sync(0xffffffffu, mk, e & 31);
-                    const int code = __shfl_sync(0xffffffffu, mcode, e & 31);
-                    const int sc = __shfl_sync(0xffffffffu, msc, e & 31);
-                    const bool diag = in && code == 3;
-                    const bool lower = in && code == (FWD ? 1 : 2);
-                    const double* vp = a.val + static_cast<int64_t>(k) * (B * B) + cr * B;
+            for (int e = 0; e < nb; ++e) {
+                const int k = __shfl_sync(0xffffffffu, mk, e);
+                const int code = __shfl_sync(0xffffffffu, mcode, e);
+                const int sc = __shfl_sync(0xffffffffu, msc, e);
+                const double* vp = a.val + static_cast<int64_t>(k) * (B * B) + cr * B;
+                if (code == 3) {
 #pragma unroll
                     for (int d = 0; d < B; ++d) {
-                        const int kl = local_of<B, FWD>(diag ? sr : sc, d, r0, r1);
-                        const bool use = (lower || (diag && (FWD ? d < cr : d > cr))) && j <= kl;
-                        cf[u][d] = use ? vp[d] : 0.0;
-                        xs[u][d] = use ? Xg[static_cast<int64_t>(kl) * (kl + 1) / 2 + j] : 0.0;
+                        if (!(FWD ? d < cr : d > cr)) continue;
+                        const int kl = local_of<B, FWD>(sr, d, r0, r1);
+                        if (j <= kl) acc -= vp[d] * Xg[static_cast<int64_t>(kl) * (kl + 1) / 2 + j];
+                    }
+                } else if (code == (FWD ? 1 : 2)) {
+                    double xs[B];
+#pragma unroll
+                    for (int d = 0; d < B; ++d) {
+                        const int kl = local_of<B, FWD>(sc, d, r0, r1);
+                        xs[d] = j <= kl ? Xg[static_cast<int64_t>(kl) * (kl + 1) / 2 + j] : 0.0;
+                    }
+#pragma unroll
+                    for (int d = 0; d < B; ++d) {
+                        const int kl = local_of<B, FWD>(sc, d, r0, r1);
+                        if (j <= kl) acc -= vp[d] * xs[d];
                     }
                 }
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-#pragma unroll
-                    for (int d = 0; d < B; ++d) acc -= cf[u][d] * xs[u][d];
             }
         }
         if (j <= i) Xg[static_cast<int64_t>(i) * (i + 1) / 2 + j] = acc * invd[static_cast<int64_t>(row) * B + cr];
