@@ -21,7 +21,7 @@
 // reference) with one barrier per level.
 //
 // T_G^-1 (lower triangular in the group's processing order, packed by rows)
-// is built by k_group_tinv: one warp per (group, 32 columns) runs the forward
+// is built by k_group_tinv: one CTA per (group, 32 columns) runs the forward
 // substitution T x = e_j for its 32 columns at once.
 #include <cuda_runtime.h>
 
@@ -323,68 +323,97 @@ __global__ void __launch_bounds__(kGT, 1) k_group_sweep(GrpArgs a, const double*
     }
 }
 
-// T_G^-1 for both directions: one warp per (group, 32 columns [j0, j0+32)),
-// forward substitution over the group's scalar rows in processing order:
-//   x_i = invd_i * (e_ij - sum_{k before i in G} a_ik x_k)
+// T_G^-1 for both directions: forward substitution over the group's scalar rows in processing order,
+//   x_i = invd_i * (e_ij - sum_{k before i in G} a_ik x_k),
+// for 32 columns [j0, j0+32) per warp (lane = column).  One scalar row step:
 template <int B, bool FWD>
-__global__ void __launch_bounds__(128) k_group_tinv(GrpArgs a, const double* __restrict__ invd,
-                                                     const int2* __restrict__ chunks, int nchunks, double* X)
+__device__ __forceinline__ void tinv_row(const GrpArgs& a, const double* __restrict__ invd, double* Xg, int r0, int r1,
+                                         int i, int j, int lane)
 {
-    const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-    const int lane = threadIdx.x % 32;
-    if (w >= nchunks) return;
-    const int g = chunks[w].x, j0 = chunks[w].y;
-    const int4 gi = a.grp[g];
-    const int r0 = gi.x, r1 = gi.y, m = gi.z;
-    double* Xg = X + a.toff[g];
-    const int j = j0 + lane;
-    for (int i = j0; i < m; ++i) {
-        const int p = i / B, cl = i % B;
-        const int sr = FWD ? r0 + p : r1 - 1 - p;
-        const int cr = FWD ? cl : B - 1 - cl;
-        const int row = a.perm ? a.perm[sr] : sr;
-        double acc = (i == j) ? 1.0 : 0.0;
-        // The row's in-group blocks: the index chain (block -> code, column -> stored row) is
-        // resolved for 32 blocks at once, one per lane, then the blocks are applied in order
-        // (the same subtraction order as a lane-serial loop) with their operands broadcast.
-        const int q0 = a.gptr[sr], q1 = a.gptr[sr + 1];
-        for (int qb = q0; qb < q1; qb += 32) {
-            int mk = 0, mcode = 0, msc = 0;
-            if (qb + lane < q1) {
-                mk = a.gblk[qb + lane];
-                mcode = a.bcode[mk];
-                const int c = a.col[mk];
-                msc = a.inv ? a.inv[c] : c;
-            }
-            const int nb = min(32, q1 - qb);
-            for (int e = 0; e < nb; ++e) {
-                const int k = __shfl_sync(0xffffffffu, mk, e);
-                const int code = __shfl_sync(0xffffffffu, mcode, e);
-                const int sc = __shfl_sync(0xffffffffu, msc, e);
-                const double* vp = a.val + static_cast<int64_t>(k) * (B * B) + cr * B;
-                if (code == 3) {
+    const int p = i / B, cl = i % B;
+    const int sr = FWD ? r0 + p : r1 - 1 - p;
+    const int cr = FWD ? cl : B - 1 - cl;
+    const int row = a.perm ? a.perm[sr] : sr;
+    double acc = (i == j) ? 1.0 : 0.0;
+    // The row's in-group blocks: the index chain (block -> code, column -> stored row) is
+    // resolved for 32 blocks at once, one per lane, then the blocks are applied in order
+    // (the same subtraction order as a lane-serial loop) with their operands broadcast.
+    const int q0 = a.gptr[sr], q1 = a.gptr[sr + 1];
+    for (int qb = q0; qb < q1; qb += 32) {
+        int mk = 0, mcode = 0, msc = 0;
+        if (qb + lane < q1) {
+            mk = a.gblk[qb + lane];
+            mcode = a.bcode[mk];
+            const int c = a.col[mk];
+            msc = a.inv ? a.inv[c] : c;
+        }
+        const int nb = min(32, q1 - qb);
+        for (int e = 0; e < nb; ++e) {
+            const int k = __shfl_sync(0xffffffffu, mk, e);
+            const int code = __shfl_sync(0xffffffffu, mcode, e);
+            const int sc = __shfl_sync(0xffffffffu, msc, e);
+            const double* vp = a.val + static_cast<int64_t>(k) * (B * B) + cr * B;
+            if (code == 3) {
 #pragma unroll
-                    for (int d = 0; d < B; ++d) {
-                        if (!(FWD ? d < cr : d > cr)) continue;
-                        const int kl = local_of<B, FWD>(sr, d, r0, r1);
-                        if (j <= kl) acc -= vp[d] * Xg[static_cast<int64_t>(kl) * (kl + 1) / 2 + j];
-                    }
-                } else if (code == (FWD ? 1 : 2)) {
-                    double xs[B];
+                for (int d = 0; d < B; ++d) {
+                    if (!(FWD ? d < cr : d > cr)) continue;
+                    const int kl = local_of<B, FWD>(sr, d, r0, r1);
+                    if (j <= kl) acc -= vp[d] * Xg[static_cast<int64_t>(kl) * (kl + 1) / 2 + j];
+                }
+            } else if (code == (FWD ? 1 : 2)) {
+                double xs[B];
 #pragma unroll
-                    for (int d = 0; d < B; ++d) {
-                        const int kl = local_of<B, FWD>(sc, d, r0, r1);
-                        xs[d] = j <= kl ? Xg[static_cast<int64_t>(kl) * (kl + 1) / 2 + j] : 0.0;
-                    }
+                for (int d = 0; d < B; ++d) {
+                    const int kl = local_of<B, FWD>(sc, d, r0, r1);
+                    xs[d] = j <= kl ? Xg[static_cast<int64_t>(kl) * (kl + 1) / 2 + j] : 0.0;
+                }
 #pragma unroll
-                    for (int d = 0; d < B; ++d) {
-                        const int kl = local_of<B, FWD>(sc, d, r0, r1);
-                        if (j <= kl) acc -= vp[d] * xs[d];
-                    }
+                for (int d = 0; d < B; ++d) {
+                    const int kl = local_of<B, FWD>(sc, d, r0, r1);
+                    if (j <= kl) acc -= vp[d] * xs[d];
                 }
             }
         }
-        if (j <= i) Xg[static_cast<int64_t>(i) * (i + 1) / 2 + j] = acc * invd[static_cast<int64_t>(row) * B + cr];
+    }
+    if (j <= i) Xg[static_cast<int64_t>(i) * (i + 1) / 2 + j] = acc * invd[static_cast<int64_t>(row) * B + cr];
+}
+
+// One CTA of kTinvWarps warps per (group, 32 columns): the block rows of one dependency level are
+// independent (their in-group couplings reach earlier levels only), so the warps split them and
+// meet at a CTA barrier per level -- the sequential depth is the group's levels (~9) times B, not
+// its scalar rows (~1000).  The B scalar rows of a block row stay with one warp, in sweep order.
+constexpr int kTinvWarps = 8;
+
+template <int B, bool FWD>
+__global__ void __launch_bounds__(32 * kTinvWarps) k_group_tinv(GrpArgs a, const double* __restrict__ invd,
+                                                                const int2* __restrict__ chunks,
+                                                                const int* __restrict__ lev_ptr, int nlev, double* X)
+{
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int g = chunks[blockIdx.x].x, j0 = chunks[blockIdx.x].y;
+    const int4 gi = a.grp[g];
+    const int r0 = gi.x, r1 = gi.y;
+    double* Xg = X + a.toff[g];
+    const int j = j0 + lane;
+    // the level that holds stored row r0 (levels are contiguous stored-row ranges; groups are whole levels)
+    int lo = 0, hi = nlev;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (lev_ptr[mid] <= r0) lo = mid;
+        else hi = mid - 1;
+    }
+    int l_first = lo, l_last = lo;
+    while (l_last + 1 < nlev && lev_ptr[l_last + 1] < r1) ++l_last;
+    const int pmin = j0 / B; // block rows (processing order) before it only hold columns left of j0: nothing to do
+    for (int li = 0; li <= l_last - l_first; ++li) {
+        const int l = FWD ? l_first + li : l_last - li;
+        const int a0 = lev_ptr[l], a1 = lev_ptr[l + 1]; // stored rows of the level
+        // processing-order positions of the level's block rows
+        const int p0 = FWD ? a0 - r0 : r1 - a1, p1 = FWD ? a1 - r0 : r1 - a0;
+        for (int pp = max(p0, pmin) + warp; pp < p1; pp += kTinvWarps)
+#pragma unroll 1
+            for (int cl = 0; cl < B; ++cl) tinv_row<B, FWD>(a, invd, Xg, r0, r1, pp * B + cl, j, lane);
+        __syncthreads();
     }
 }
 
@@ -452,13 +481,15 @@ void group_prepare(const Bsr& A, const double* invd, DevArray<double>& X, cudaSt
     }
     X.alloc(2 * static_cast<size_t>(S.grp_tinv));
     const GrpArgs a = gargs_of(A);
-    const int blocks = (S.ntchunk * 32 + 127) / 128;
+    const int nlev = S.nlev();
     if (S.Rb == 3) {
-        k_group_tinv<3, true><<<blocks, 128, 0, s>>>(a, invd, S.tchunk.p, S.ntchunk, X.p);
-        k_group_tinv<3, false><<<blocks, 128, 0, s>>>(a, invd, S.tchunk.p, S.ntchunk, X.p + S.grp_tinv);
+        k_group_tinv<3, true><<<S.ntchunk, 32 * kTinvWarps, 0, s>>>(a, invd, S.tchunk.p, S.d_lev_ptr.p, nlev, X.p);
+        k_group_tinv<3, false><<<S.ntchunk, 32 * kTinvWarps, 0, s>>>(a, invd, S.tchunk.p, S.d_lev_ptr.p, nlev,
+                                                                     X.p + S.grp_tinv);
     } else {
-        k_group_tinv<1, true><<<blocks, 128, 0, s>>>(a, invd, S.tchunk.p, S.ntchunk, X.p);
-        k_group_tinv<1, false><<<blocks, 128, 0, s>>>(a, invd, S.tchunk.p, S.ntchunk, X.p + S.grp_tinv);
+        k_group_tinv<1, true><<<S.ntchunk, 32 * kTinvWarps, 0, s>>>(a, invd, S.tchunk.p, S.d_lev_ptr.p, nlev, X.p);
+        k_group_tinv<1, false><<<S.ntchunk, 32 * kTinvWarps, 0, s>>>(a, invd, S.tchunk.p, S.d_lev_ptr.p, nlev,
+                                                                     X.p + S.grp_tinv);
     }
     after_launch("k_group_tinv");
 }
