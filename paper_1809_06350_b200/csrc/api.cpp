@@ -501,6 +501,7 @@ int ed_mesh_upload(ed_ctx* ctx, int n_nodes, int n_tets, const int32_t* tets, co
 int ed_dofs_build(ed_ctx* ctx, const uint8_t* fixed, int32_t* nv, int32_t* np)
 {
     return guarded(ctx, [&](Ctx& c) {
+        c.pd_n = 0; // a pending prescription refers to the previous constraint set
         check(c.have_mesh, ED_NOT_READY, "mesh required");
         check(fixed != nullptr, ED_INVALID_ARGUMENT, "DofMap: constraint table missing");
         const int N = c.n_nodes;
