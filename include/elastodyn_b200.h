@@ -237,6 +237,12 @@ int ed_step_generalized_alpha(ed_ctx* ctx, const ed_time_scalars* ts, const ed_n
 /* y = K x (BlockMatrix::matvec, blocksystem.hpp:27-33) on the current system
  * (unscaled), host vectors of length nv+np. */
 int ed_block_matvec(ed_ctx* ctx, const double* x, double* y);
+/* The same product on the solver's working copy of the current mesh system (scaled when
+ * opts->scale, blocksystem.cpp:79-106), through the coupled 4x4 BSR operator the outer FGMRES
+ * uses (y_coupled) and through the four BSR planes (y_planes): kernel-level parity of the two
+ * storages of K. */
+int ed_coupled_matvec(ed_ctx* ctx, const ed_block_solver_options* opts, const double* x,
+                      double* y_coupled, double* y_planes);
 /* gmres/fgmres (krylov.cpp:180-192) on the current A block (unscaled), with
  * precond 0 none, 1 Jacobi, 2 AMG(amg).  x holds the initial guess. */
 int ed_gmres_a(ed_ctx* ctx, const double* b, double* x, const ed_krylov_config* cfg,

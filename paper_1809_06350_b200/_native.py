@@ -28,7 +28,7 @@ EXPORTED = [
     "ed_solve_block_system_device", "ed_newton_first_pass", "ed_step_generalized_alpha", "ed_block_matvec", "ed_gmres_a",
     "ed_amg_vcycle", "ed_shat_export", "ed_block_matvec_device", "ed_spmv_bytes", "ed_state_save",
     "ed_state_restore", "ed_timer", "ed_bench_kernels", "ed_bench_assembly", "ed_kernel_accounting", "ed_kernel_account_count",
-    "ed_kernel_account_get", "ed_set_fiber_field", "ed_set_prescribed_displacement",
+    "ed_kernel_account_get", "ed_set_fiber_field", "ed_set_prescribed_displacement", "ed_coupled_matvec",
 ]
 
 
@@ -129,6 +129,7 @@ def lib():
         "ed_set_material": (C.c_int, [P, C.POINTER(Material)]),
         "ed_set_loads": (C.c_int, [P, dp, C.c_int, ip, dp, dp]),
         "ed_set_fiber_field": (C.c_int, [P, C.c_int, dp]),
+        "ed_coupled_matvec": (C.c_int, [P, C.POINTER(BlockSolverOptions), dp, dp, dp]),
         "ed_set_prescribed_displacement": (C.c_int, [P, C.c_int, ip, dp]),
         "ed_state_upload": (C.c_int, [P] + [dp] * 6),
         "ed_state_download": (C.c_int, [P] + [dp] * 6),

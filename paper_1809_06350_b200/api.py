@@ -345,6 +345,14 @@ class Context:
         self._chk(N.lib().ed_block_matvec(self._p, N.dp(N.f64(x)), N.dp(y)))
         return y
 
+    def coupled_matvec(self, x, opts: N.BlockSolverOptions | None = None):
+        """K x on the solver's working copy through the coupled 4x4 BSR operator and through the planes."""
+        opts = opts or block_solver_options()
+        xx = N.f64(x)
+        y1, y2 = np.zeros(xx.size), np.zeros(xx.size)
+        self._chk(N.lib().ed_coupled_matvec(self._p, C.byref(opts), N.dp(xx), N.dp(y1), N.dp(y2)))
+        return y1, y2
+
     def gmres_a(self, b, x0=None, cfg=None, flexible=False, precond=0, amg=None, hist_cap=100000):
         """gmres/fgmres (krylov.cpp:180-192) on the A block; precond 0 none,
         1 JacobiPrecond (krylov.hpp:51-62), 2 AmgPrecond (amg.hpp:76-89)."""

@@ -1014,6 +1014,28 @@ int ed_block_matvec(ed_ctx* ctx, const double* x, double* y)
     });
 }
 
+int ed_coupled_matvec(ed_ctx* ctx, const ed_block_solver_options* opts, const double* x, double* y_coupled,
+                      double* y_planes)
+{
+    return guarded(ctx, [&](Ctx& c) {
+        check(opts && x && y_coupled && y_planes, ED_INVALID_ARGUMENT, "bad arguments");
+        ensure_system(c, opts);
+        WorkSys& W = c.work;
+        make_work(c, W, opts->scale != 0, opts->eps_diag);
+        check(W.K.n_nodes > 0, ED_NOT_READY, "no coupled operator (the system was not assembled from a mesh)");
+        const int nv = W.nv;
+        const size_t n = static_cast<size_t>(nv) + W.np;
+        DevArray<double> xd, y1(n), y2(n);
+        xd.upload(x, n, c.stream);
+        spmv44(W.K, xd.p, y1.p, nv, W.np, c.stream);
+        spmv2(W.A, xd.p, W.B, xd.p + nv, y2.p, 1.0, c.stream);
+        spmv2(W.C, xd.p, W.D, xd.p + nv, y2.p + nv, 1.0, c.stream);
+        y1.download(y_coupled, c.stream);
+        y2.download(y_planes, c.stream);
+        c.sync();
+    });
+}
+
 int ed_block_matvec_device(ed_ctx* ctx, const double* d_x, double* d_y, int n_rep, float* ms)
 {
     return guarded(ctx, [&](Ctx& c) {

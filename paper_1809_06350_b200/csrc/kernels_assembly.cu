@@ -17,6 +17,7 @@
 // unstable sort (csr.cpp:84-87), hence parity is at roundoff level.
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -28,8 +29,7 @@ namespace edb {
 namespace {
 
 constexpr int kTeam = 16;
-constexpr int kTeamsPerCta = 8;
-constexpr int kCta = kTeam * kTeamsPerCta;
+
 
 // 4-point degree-2 rule (quadrature.hpp:18-26)
 __constant__ double c_qa = 0.5854101966249685;
@@ -187,6 +187,8 @@ struct Frame {
     int nodes[4];
     int free_idx[4];
     int valid;
+    int active; // the team has an element
+    int elem;   // its element id
 };
 
 // ptilde_dir (materials.cpp:108-129) for dF = e_j (x) G_b
@@ -241,170 +243,204 @@ __device__ void ptilde_dir(const ed_material& m, const Frame& f, int bn, int j, 
     for (int k = 0; k < 9; ++k) out[k] = b1[k] + 1.0 * b2[k];
 }
 
-// Phases A-C shared by residual and tangent kernels.  All lanes of the CTA
-// call it (it contains __syncthreads).  Returns with f.valid == 0 for an
-// inactive team or an inverted element.
-__device__ void build_frame(const AsmArgs& A, Frame& f, int e, int lane, bool active, bool with_rk)
+// Phases A-C shared by residual and tangent kernels, for the kTeamsPerCta
+// elements of a CTA at once.  The per-element serial work (kinematics, stress,
+// div v / L / grad p, quadrature-point data) is ROLE-MAJOR: thread t of the CTA
+// does job t / T for element t % T (T = 8 elements per CTA), so a warp that
+// issues FP64 instructions in these phases has all 32 lanes active and the
+// other warps wait at the CTA barrier.  (A predicated-off lane costs the FP64
+// pipe as much as an active one; with team-local lanes 0..3 doing this work the
+// serial phases ran at 1-4 active lanes of 16.  160^3: residual 23.7 -> 17.5 ms,
+// tangent 103.2 -> 99.6 ms; 16 or 32 elements per CTA lose the overlap between
+// CTAs and are slower for the tangent, profiles/r02/assembly_experiments.md.)
+// The arithmetic per element is unchanged.
+// All threads of the CTA call it (it contains __syncthreads); f.valid == 0
+// afterwards for an inactive team or an inverted element.
+template <int T>
+__device__ void build_frames(const AsmArgs& A, Frame* frames, int c0, int count, bool with_rk)
 {
-    // --- A: gather
-    if (active && lane < 4) {
-        const int a = lane;
-        const int n = A.tets[4 * static_cast<int64_t>(e) + a];
-        f.nodes[a] = n;
-        f.free_idx[a] = A.fidx[n];
+    const int t = threadIdx.x;
+    // --- A: gather (thread = (element, node))
+    if (t < 4 * T) {
+        const int team = t >> 2, a = t & 3;
+        Frame& f = frames[team];
+        const int idx = blockIdx.x * T + team;
+        const bool active = idx < count;
+        if (a == 0) f.active = active;
+        if (active) {
+            const int e = A.elem_order[c0 + idx];
+            const int n = A.tets[4 * static_cast<int64_t>(e) + a];
+            f.nodes[a] = n;
+            const int fi = A.fidx[n];
+            f.free_idx[a] = fi;
 #pragma unroll
-        for (int I = 0; I < 3; ++I) f.G[a][I] = A.grad_n[12 * static_cast<int64_t>(e) + 3 * a + I];
+            for (int I = 0; I < 3; ++I) f.G[a][I] = A.grad_n[12 * static_cast<int64_t>(e) + 3 * a + I];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            f.u[a][i] = A.u[3 * static_cast<int64_t>(n) + i];
-            f.v[a][i] = A.v[3 * static_cast<int64_t>(n) + i];
-            f.vd[a][i] = A.vdot[3 * static_cast<int64_t>(n) + i];
-            f.rk[a][i] = (with_rk && A.rk && f.free_idx[a] >= 0) ? A.rk[3 * static_cast<int64_t>(f.free_idx[a]) + i]
-                                                                 : 0.0;
-        }
-        f.pe[a] = A.p[n];
-        f.pde[a] = A.pdot[n];
-    }
-    if (active && lane == 4) {
-        f.vol = A.volume[e];
-        f.tau = A.tau[e];
-    }
-    if (active && A.mat.kind == 1 && (lane == 5 || lane == 6)) {
-        // per-element fibre field (local frames) or the material's global tensors
-        const int fam = lane - 5;
-        const double* H = A.elem_h ? A.elem_h + 18 * static_cast<int64_t>(e) + 9 * fam : (fam ? A.mat.h2 : A.mat.h1);
-#pragma unroll
-        for (int k = 0; k < 9; ++k) f.H[fam][k] = H[k];
-    }
-    __syncthreads();
-    // --- B: kinematics + stress (Kinematics::from_F, evaluate_stress).  The
-    // three independent chains -- F^-1; C = F^T F and C^-1; J^-2/3 -- run on
-    // lanes 0, 1, 2 (each recomputes F and J identically), then lane 0 forms
-    // the stresses.
-    if (active && lane < 3) {
-        double F[9] = {1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0};
-        for (int a = 0; a < 4; ++a)
-            for (int i = 0; i < 3; ++i)
-                for (int I = 0; I < 3; ++I) F[3 * i + I] = F[3 * i + I] + f.u[a][i] * f.G[a][I];
-        const double J = det3(F);
-        if (!(J > 0.0)) {
-            if (lane == 0) {
-                f.valid = 0;
-                atomicMin(A.bad_element, e);
-            }
-        } else if (lane == 0) {
-            f.valid = 1;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) f.F[k] = F[k];
-            f.J = J;
-            inv3(F, f.Finv);
-        } else if (lane == 1) {
-            matTmul3(F, F, f.C);
-            inv3(f.C, f.Cinv);
-        } else {
-            f.Jm23 = pow(J, -2.0 / 3.0);
-        }
-    } else if (lane == 0) {
-        f.valid = 0;
-    }
-    __syncthreads();
-    if (f.valid && lane == 0) {
-#pragma unroll
-        for (int k = 0; k < 9; ++k) f.Ct[k] = f.C[k] * f.Jm23;
-        iso_stress(A.mat, f.H, f.Ct, f.St);
-        const double sc = ddot3(f.St, f.Ct);
-        const double c1 = -sc / 3.0;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) f.Siso[k] = f.St[k] * f.Jm23 + c1 * f.Cinv[k];
-        matmul3(f.F, f.Siso, f.Pt);
-    }
-    __syncthreads();
-    if (!f.valid) return;
-    // --- C1: spatial gradients g_a = F^-T G_a (tmulvec3)
-    if (lane < 4) {
-        const int a = lane;
-        const double* m = f.Finv;
-        const double* x = f.G[a];
-        f.g[a][0] = m[0] * x[0] + m[3] * x[1] + m[6] * x[2];
-        f.g[a][1] = m[1] * x[0] + m[4] * x[1] + m[7] * x[2];
-        f.g[a][2] = m[2] * x[0] + m[5] * x[1] + m[8] * x[2];
-    }
-    __syncwarp();
-    // --- C2: div v, L, grad p (lane 0), quadrature-point values (lanes 4..7)
-    if (lane == 0) {
-        double divv = 0.0, gp[3] = {0.0, 0.0, 0.0}, L[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) L[k] = 0.0;
-        for (int a = 0; a < 4; ++a) {
-            divv = divv + dot3(f.v[a], f.g[a]);
             for (int i = 0; i < 3; ++i) {
-                gp[i] = gp[i] + f.pe[a] * f.g[a][i];
-                for (int j = 0; j < 3; ++j) L[3 * i + j] = L[3 * i + j] + f.v[a][i] * f.g[a][j];
+                f.u[a][i] = A.u[3 * static_cast<int64_t>(n) + i];
+                f.v[a][i] = A.v[3 * static_cast<int64_t>(n) + i];
+                f.vd[a][i] = A.vdot[3 * static_cast<int64_t>(n) + i];
+                f.rk[a][i] = (with_rk && A.rk && fi >= 0) ? A.rk[3 * static_cast<int64_t>(fi) + i] : 0.0;
+            }
+            f.pe[a] = A.p[n];
+            f.pde[a] = A.pdot[n];
+            if (a == 0) {
+                f.elem = e;
+                f.vol = A.volume[e];
+                f.tau = A.tau[e];
+            }
+            if (A.mat.kind == 1 && a >= 1 && a <= 2) {
+                // per-element fibre field (local frames) or the material's global tensors
+                const int fam = a - 1;
+                const double* H =
+                    A.elem_h ? A.elem_h + 18 * static_cast<int64_t>(e) + 9 * fam : (fam ? A.mat.h2 : A.mat.h1);
+#pragma unroll
+                for (int k = 0; k < 9; ++k) f.H[fam][k] = H[k];
             }
         }
-        f.divv = divv;
-#pragma unroll
-        for (int i = 0; i < 3; ++i) f.gp[i] = gp[i];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) f.L[k] = L[k];
     }
-    if (lane >= 4 && lane < 8) {
-        const int q = lane - 4;
-        double pq = 0.0, pdq = 0.0, vdq[3] = {0.0, 0.0, 0.0};
-        for (int a = 0; a < 4; ++a) {
-            const double Na = bary(q, a);
-            pq = pq + Na * f.pe[a];
-            pdq = pdq + Na * f.pde[a];
-            for (int i = 0; i < 3; ++i) vdq[i] = vdq[i] + Na * f.vd[a][i];
+    __syncthreads();
+    // --- B: kinematics (Kinematics::from_F).  The three independent chains -- F^-1; C = F^T F
+    // and C^-1; J^-2/3 -- are jobs 0, 1, 2 (each recomputes F and J identically).
+    if (t < 3 * T) {
+        const int job = t / T;
+        Frame& f = frames[t % T];
+        if (f.active) {
+            double F[9] = {1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0};
+            for (int a = 0; a < 4; ++a)
+                for (int i = 0; i < 3; ++i)
+                    for (int I = 0; I < 3; ++I) F[3 * i + I] = F[3 * i + I] + f.u[a][i] * f.G[a][I];
+            const double J = det3(F);
+            if (!(J > 0.0)) {
+                if (job == 0) {
+                    f.valid = 0;
+                    atomicMin(A.bad_element, f.elem);
+                }
+            } else if (job == 0) {
+                f.valid = 1;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) f.F[k] = F[k];
+                f.J = J;
+                inv3(F, f.Finv);
+            } else if (job == 1) {
+                matTmul3(F, F, f.C);
+                inv3(f.C, f.Cinv);
+            } else {
+                f.Jm23 = pow(J, -2.0 / 3.0);
+            }
+        } else if (job == 0) {
+            f.valid = 0;
         }
-        f.pq[q] = pq;
-        f.pdq[q] = pdq;
+    }
+    __syncthreads();
+    // --- stress (evaluate_stress) and C1: spatial gradients g_a = F^-T G_a (tmulvec3), jobs 1..4
+    if (t < T) {
+        Frame& f = frames[t];
+        if (f.valid) {
 #pragma unroll
-        for (int i = 0; i < 3; ++i) f.vdq[q][i] = vdq[i];
-        const Vol vm = volumetric(A.mat, pq);
-        f.rho[q] = vm.rho;
-        f.beta[q] = vm.beta;
-        f.drho[q] = vm.drho;
-        f.dbeta[q] = vm.dbeta;
-    }
-    __syncwarp();
-    // --- C3: strong residual terms per quadrature point (lanes 4..7), pbar
-    if (lane >= 4 && lane < 8) {
-        const int q = lane - 4;
-        const double J = f.J;
+            for (int k = 0; k < 9; ++k) f.Ct[k] = f.C[k] * f.Jm23;
+            iso_stress(A.mat, f.H, f.Ct, f.St);
+            const double sc = ddot3(f.St, f.Ct);
+            const double c1 = -sc / 3.0;
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            f.vmb[q][i] = f.vdq[q][i] - A.body_force[i];
-            f.res[q][i] = f.rho[q] * J * f.vmb[q][i] + J * f.gp[i];
+            for (int k = 0; k < 9; ++k) f.Siso[k] = f.St[k] * f.Jm23 + c1 * f.Cinv[k];
+            matmul3(f.F, f.Siso, f.Pt);
         }
-        f.cont[q] = J * (f.beta[q] * f.pdq[q] + f.divv);
-    }
-    if (lane == 0) {
-        // pbar += w_q * pq with w_q = 1/4, q ascending (assembly.cpp:142); pq
-        // is recomputed here in the same order as lanes 4..7 did
-        double pbar = 0.0;
-        for (int q = 0; q < 4; ++q) {
-            double pq = 0.0;
-            for (int a = 0; a < 4; ++a) pq = pq + bary(q, a) * f.pe[a];
-            pbar = pbar + 0.25 * pq;
+    } else if (t < 5 * T) {
+        Frame& f = frames[t % T];
+        if (f.valid) {
+            const int a = t / T - 1;
+            const double* m = f.Finv;
+            const double* x = f.G[a];
+            f.g[a][0] = m[0] * x[0] + m[3] * x[1] + m[6] * x[2];
+            f.g[a][1] = m[1] * x[0] + m[4] * x[1] + m[7] * x[2];
+            f.g[a][2] = m[2] * x[0] + m[5] * x[1] + m[8] * x[2];
         }
-        f.pbar = pbar;
     }
-    __syncwarp();
+    __syncthreads();
+    // --- C2: div v, L, grad p (job 0), quadrature-point values (jobs 1..4)
+    if (t < T) {
+        Frame& f = frames[t];
+        if (f.valid) {
+            double divv = 0.0, gp[3] = {0.0, 0.0, 0.0}, L[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) L[k] = 0.0;
+            for (int a = 0; a < 4; ++a) {
+                divv = divv + dot3(f.v[a], f.g[a]);
+                for (int i = 0; i < 3; ++i) {
+                    gp[i] = gp[i] + f.pe[a] * f.g[a][i];
+                    for (int j = 0; j < 3; ++j) L[3 * i + j] = L[3 * i + j] + f.v[a][i] * f.g[a][j];
+                }
+            }
+            f.divv = divv;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) f.gp[i] = gp[i];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) f.L[k] = L[k];
+        }
+    } else if (t < 5 * T) {
+        Frame& f = frames[t % T];
+        if (f.valid) {
+            const int q = t / T - 1;
+            double pq = 0.0, pdq = 0.0, vdq[3] = {0.0, 0.0, 0.0};
+            for (int a = 0; a < 4; ++a) {
+                const double Na = bary(q, a);
+                pq = pq + Na * f.pe[a];
+                pdq = pdq + Na * f.pde[a];
+                for (int i = 0; i < 3; ++i) vdq[i] = vdq[i] + Na * f.vd[a][i];
+            }
+            f.pq[q] = pq;
+            f.pdq[q] = pdq;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) f.vdq[q][i] = vdq[i];
+            const Vol vm = volumetric(A.mat, pq);
+            f.rho[q] = vm.rho;
+            f.beta[q] = vm.beta;
+            f.drho[q] = vm.drho;
+            f.dbeta[q] = vm.dbeta;
+        }
+    }
+    __syncthreads();
+    // --- C3: strong residual terms per quadrature point (jobs 1..4), pbar (job 0)
+    if (t < T) {
+        Frame& f = frames[t];
+        if (f.valid) {
+            // pbar += w_q * pq with w_q = 1/4, q ascending (assembly.cpp:142); pq
+            // is recomputed here in the same order as the quadrature jobs did
+            double pbar = 0.0;
+            for (int q = 0; q < 4; ++q) {
+                double pq = 0.0;
+                for (int a = 0; a < 4; ++a) pq = pq + bary(q, a) * f.pe[a];
+                pbar = pbar + 0.25 * pq;
+            }
+            f.pbar = pbar;
+        }
+    } else if (t < 5 * T) {
+        Frame& f = frames[t % T];
+        if (f.valid) {
+            const int q = t / T - 1;
+            const double J = f.J;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                f.vmb[q][i] = f.vdq[q][i] - A.body_force[i];
+                f.res[q][i] = f.rho[q] * J * f.vmb[q][i] + J * f.gp[i];
+            }
+            f.cont[q] = J * (f.beta[q] * f.pdq[q] + f.divv);
+        }
+    }
+    __syncthreads();
 }
 
 // Residual kernel: lane = 4a + c, c < 3 -> R_m[a][c], c == 3 -> R_p[a].
-template <int MINB>
-__global__ void __launch_bounds__(kCta, MINB) k_residual(AsmArgs A, int c0, int count)
+template <int T, bool R64>
+__global__ void __launch_bounds__(kTeam * T, (R64 ? 1024 : 512) / (kTeam * T)) k_residual(AsmArgs A, int c0, int count)
 {
-    __shared__ Frame frames[kTeamsPerCta];
+    extern __shared__ __align__(16) unsigned char frame_smem[];
+    Frame* frames = reinterpret_cast<Frame*>(frame_smem);
     const int team = threadIdx.x / kTeam;
     const int lane = threadIdx.x % kTeam;
-    const int idx = blockIdx.x * kTeamsPerCta + team;
-    const bool active = idx < count;
-    const int e = active ? A.elem_order[c0 + idx] : 0;
     Frame& f = frames[team];
-    build_frame(A, f, e, lane, active, false);
+    build_frames<T>(A, frames, c0, count, false);
     if (!f.valid) return;
     const int a = lane / 4, c = lane % 4;
     const double J = f.J;
@@ -436,13 +472,14 @@ __global__ void __launch_bounds__(kCta, MINB) k_residual(AsmArgs A, int c0, int 
 
 // Tangent kernel: dP for 12 directions, then lane = 4a + bn forms node block
 // (a, bn) of eA, eB, eC, eD (+ eM, eK for the fold-in).
-template <int MINB>
-__global__ void __launch_bounds__(kCta, MINB) k_tangent(AsmArgs A, int c0, int count)
+template <int T, bool R64>
+__global__ void __launch_bounds__(kTeam * T, (R64 ? 1024 : 512) / (kTeam * T)) k_tangent(AsmArgs A, int c0, int count)
 {
-    __shared__ Frame frames[kTeamsPerCta];
+    extern __shared__ __align__(16) unsigned char frame_smem[];
+    Frame* frames = reinterpret_cast<Frame*>(frame_smem);
     const int team = threadIdx.x / kTeam;
     const int lane = threadIdx.x % kTeam;
-    const int idx = blockIdx.x * kTeamsPerCta + team;
+    const int idx = blockIdx.x * T + team;
     const bool active = idx < count;
     const int e = active ? A.elem_order[c0 + idx] : 0;
     Frame& f = frames[team];
@@ -450,7 +487,7 @@ __global__ void __launch_bounds__(kCta, MINB) k_tangent(AsmArgs A, int c0, int c
     // start pulling its line into L1 now, behind the element's arithmetic
     const int kslot = active ? A.k4slot[16 * static_cast<int64_t>(e) + lane] : 0;
     if (active) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.k4 + 16 * static_cast<int64_t>(kslot)));
-    build_frame(A, f, e, lane, active, true);
+    build_frames<T>(A, frames, c0, count, true);
     if (!f.valid) return;
     if (lane < 12) ptilde_dir(A.mat, f, lane / 3, lane % 3, f.dP[lane]);
     __syncwarp();
@@ -651,74 +688,41 @@ void launch_k4_split(const double* k4, const int* dstA, const int* dstB, const i
     after_launch("k_k4_split");
 }
 
-// resident CTAs per SM the element kernels are compiled for (register cap);
-// ED_ASM_MINB=<residual><tangent> picks a variant (experiments), e.g. 86
-int asm_minb(int which)
-{
-    // measured at 160^3 (round-1 ED_ASM_MINB scan with scripts/asm_probe.py): residual 8 CTAs/SM (64
-    // registers), tangent 4 (128 registers, no spills)
-    const char* e = std::getenv("ED_ASM_MINB");
-    const int v = e ? std::atoi(e) : 84;
-    return which == 0 ? v / 10 : v % 10;
-}
+// Eight elements per 128-thread CTA (measured against 16 and 32 at 160^3,
+// profiles/r02/assembly_experiments.md); the residual is compiled for 64 registers per thread (8 CTAs
+// per SM), the tangent for 128 (4 CTAs per SM, no spills to speak of).
+constexpr int kTeamsPerCta = 8;
+constexpr int kCta = kTeam * kTeamsPerCta;
+constexpr size_t kFrameBytes = sizeof(Frame) * kTeamsPerCta; // dynamic shared memory per CTA
 
-// the frames are 22 KB of static shared memory per CTA: ask for the largest
-// shared-memory carveout so the register cap, not the carveout, sets residency
 template <typename K>
-void max_carveout(K kernel)
+void launch_elements(K kernel, const char* name, const AsmArgs& A, const std::vector<int>& color_ptr, cudaStream_t s)
 {
-    ED_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 cudaSharedmemCarveoutMaxShared));
-}
-
-#define ED_ASM_LAUNCH(KER, MB, ...)                                                                            \
-    switch (MB) {                                                                                              \
-    case 4: KER<4><<<__VA_ARGS__>>>(A, color_ptr[c], count); break;                                           \
-    case 5: KER<5><<<__VA_ARGS__>>>(A, color_ptr[c], count); break;                                           \
-    case 6: KER<6><<<__VA_ARGS__>>>(A, color_ptr[c], count); break;                                           \
-    case 8: KER<8><<<__VA_ARGS__>>>(A, color_ptr[c], count); break;                                           \
-    default: KER<1><<<__VA_ARGS__>>>(A, color_ptr[c], count); break;                                          \
+    static bool done[64] = {}; // per kernel instantiation and device
+    int dev = 0;
+    ED_CUDA(cudaGetDevice(&dev));
+    if (!done[dev & 63]) {
+        ED_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kFrameBytes)));
+        ED_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared));
+        done[dev & 63] = true;
     }
-
-void carveouts()
-{
-    static std::once_flag once;
-    std::call_once(once, [] {
-        max_carveout(k_residual<1>);
-        max_carveout(k_residual<4>);
-        max_carveout(k_residual<5>);
-        max_carveout(k_residual<6>);
-        max_carveout(k_residual<8>);
-        max_carveout(k_tangent<1>);
-        max_carveout(k_tangent<4>);
-        max_carveout(k_tangent<5>);
-        max_carveout(k_tangent<6>);
-        max_carveout(k_tangent<8>);
-    });
+    for (size_t c = 0; c + 1 < color_ptr.size(); ++c) {
+        const int count = color_ptr[c + 1] - color_ptr[c];
+        if (count == 0) continue;
+        kernel<<<(count + kTeamsPerCta - 1) / kTeamsPerCta, kCta, kFrameBytes, s>>>(A, color_ptr[c], count);
+        after_launch(name);
+    }
 }
 
 void launch_residual(const AsmArgs& A, const std::vector<int>& color_ptr, cudaStream_t s)
 {
-    carveouts();
-    const int mb = asm_minb(0);
-    for (size_t c = 0; c + 1 < color_ptr.size(); ++c) {
-        const int count = color_ptr[c + 1] - color_ptr[c];
-        if (count == 0) continue;
-        ED_ASM_LAUNCH(k_residual, mb, (count + kTeamsPerCta - 1) / kTeamsPerCta, kCta, 0, s)
-        after_launch("k_residual");
-    }
+    launch_elements(k_residual<kTeamsPerCta, true>, "k_residual", A, color_ptr, s);
 }
 
 void launch_tangent(const AsmArgs& A, const std::vector<int>& color_ptr, cudaStream_t s)
 {
-    carveouts();
-    const int mb = asm_minb(1);
-    for (size_t c = 0; c + 1 < color_ptr.size(); ++c) {
-        const int count = color_ptr[c + 1] - color_ptr[c];
-        if (count == 0) continue;
-        ED_ASM_LAUNCH(k_tangent, mb, (count + kTeamsPerCta - 1) / kTeamsPerCta, kCta, 0, s)
-        after_launch("k_tangent");
-    }
+    launch_elements(k_tangent<kTeamsPerCta, false>, "k_tangent", A, color_ptr, s);
 }
 
 void launch_traction(const int64_t* rowptr, const int* rows, const double* vals, int nrows_with, double* r_m,

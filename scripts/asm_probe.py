@@ -17,8 +17,5 @@ ctx.set_state(cp.seeded_state())
 ctx.assemble_residuals()
 ctx.assemble_tangent(cp.ts)
 if os.environ.get("ASM_BENCH", "1") == "1":
-    # ASM_VARIANTS="0 44 55": element-kernel register-cap variants (ED_ASM_MINB)
-    for v in os.environ.get("ASM_VARIANTS", "0").split():
-        os.environ["ED_ASM_MINB"] = v
-        r = ctx.bench_assembly(cp.ts, n_rep=3)
-        print(json.dumps(dict(n=n, tets=cp.mesh.n_tets, variant=v, **r)), flush=True)
+    r = ctx.bench_assembly(cp.ts, n_rep=3)
+    print(json.dumps(dict(n=n, tets=cp.mesh.n_tets, **r)), flush=True)

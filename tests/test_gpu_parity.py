@@ -139,6 +139,28 @@ def test_block_matvec_bitwise(cfg0):
     assert _rel(y, ref_y) < 1e-14
 
 
+@pytest.mark.parametrize("scale", [0, 1])
+def test_coupled_operator_matches_planes_and_reference(cfg0, scale):
+    """The coupled 4x4 BSR operator of the outer FGMRES (k_spmv44) against the four planes on the
+    solver's working copy, and, unscaled, against the reference's BlockMatrix::matvec on the
+    reference's own tangent (blocksystem.hpp:27-33)."""
+    cp, P, st, planes = cfg0
+    ctx = cp.context(0)
+    ctx.set_state(st)
+    ctx.assemble_residuals()
+    ctx.assemble_tangent(cp.ts)
+    x = np.random.default_rng(3).uniform(-1, 1, cp.nv + cp.np)
+    opts = cp.solver_options()
+    opts.scale = scale
+    yc, yp = ctx.coupled_matvec(x, opts)
+    assert _rel(yc, yp) < 1e-14
+    if not scale:
+        A, B, Cm, D = [m.to_scipy() for m in planes]
+        ref_y = np.concatenate([A @ x[: cp.nv] + B @ x[cp.nv:], Cm @ x[: cp.nv] + D @ x[cp.nv:]])
+        assert _rel(yc, ref_y) < 1e-12
+    ctx.close()
+
+
 def test_gmres_on_A_matches_reference(cfg0, oracle):
     cp, P, st, planes = cfg0
     ctx = api.Context(0)
