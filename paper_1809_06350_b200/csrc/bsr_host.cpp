@@ -207,6 +207,14 @@ void group_build(BsrStruct& S, cudaStream_t s)
     // tagged dataflow sweep, which needs no grid-wide barrier per level
     static const int max_rpl = std::getenv("ED_GROUP_MAX_RPL") ? std::atoi(std::getenv("ED_GROUP_MAX_RPL")) : 64;
     S.grp_use = nlev > 0 && static_cast<double>(n) / nlev <= max_rpl && tot > 0;
+    // dense-row levels (hundreds of blocks per row; the Galerkin products at 160^3): the whole CTA
+    // works on one row at a time, so a row's blocks are in flight together (ED_GROUP_WIDE_ROW:
+    // average blocks per row from which on, default 192)
+    {
+        const char* e = std::getenv("ED_GROUP_WIDE_ROW");
+        const double wide = e ? std::atof(e) : 192.0;
+        if (S.grp_use && n > 0 && static_cast<double>(S.nnzb) / n >= wide) S.Ls = 256;
+    }
     S.ntchunk = static_cast<int>(chunks.size());
     const bool identity = S.h_inv.empty();
     std::vector<unsigned char> code(S.nnzb, 0);

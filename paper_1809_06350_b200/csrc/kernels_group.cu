@@ -95,6 +95,32 @@ __device__ __forceinline__ double lane_sum(double v)
     return v;
 }
 
+// Row sums over a whole CTA (L = kGT lanes per row: dense-row coarse levels with hundreds of blocks
+// per row): warp shuffles, then the eight warp partials through shared memory, summed by thread 0
+// in warp order.  All threads of the CTA call it.
+template <int B>
+__device__ __forceinline__ void cta_sum(double (&acc)[B])
+{
+    __shared__ double red[kGT / 32][B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) acc[r] = lane_sum<32>(acc[r]);
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int r = 0; r < B; ++r) red[threadIdx.x / 32][r] = acc[r];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+            double t = red[0][r];
+#pragma unroll
+            for (int w = 1; w < kGT / 32; ++w) t += red[w][r];
+            acc[r] = t;
+        }
+    }
+    __syncthreads();
+}
+
 // local index (processing order) of scalar (stored row sr, component c) in group [r0, r1)
 template <int B, bool FWD>
 __device__ __forceinline__ int local_of(int sr, int c, int r0, int r1)
@@ -212,7 +238,12 @@ __device__ __forceinline__ void grow_finish(const GrpArgs& a, double* z, double*
                     if (codeb[p] >= 0 && takes<FWD, MULTI>(codeb[p], r, d)) acc[r] = fma(vb[p][r * B + d], zb[p][d], acc[r]);
     }
 #pragma unroll
-    for (int r = 0; r < B; ++r) acc[r] = lane_sum<L>(acc[r]);
+    if (L > 32) {
+        cta_sum<B>(acc);
+    } else {
+#pragma unroll
+        for (int r = 0; r < B; ++r) acc[r] = lane_sum<(L > 32 ? 32 : L)>(acc[r]);
+    }
     if (!P.valid || lane != 0) return;
     if (MULTI) {
 #pragma unroll
@@ -450,6 +481,7 @@ int sweep_grid()
     case 4: { constexpr int LL = 4; __VA_ARGS__; break; }   \
     case 8: { constexpr int LL = 8; __VA_ARGS__; break; }   \
     case 16: { constexpr int LL = 16; __VA_ARGS__; break; } \
+    case 256: { constexpr int LL = 256; __VA_ARGS__; break; } \
     default: { constexpr int LL = 32; __VA_ARGS__; break; } \
     }
 

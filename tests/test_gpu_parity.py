@@ -718,3 +718,27 @@ def test_prescribing_the_current_boundary_state_is_the_homogeneous_step():
     assert np.array_equal(outs[0][0]["res_history"], outs[1][0]["res_history"])
     for key in ("u", "udot", "p", "pdot", "v", "vdot"):
         assert np.array_equal(getattr(outs[0][1], key), getattr(outs[1][1], key)), key
+
+
+def test_group_sweep_with_cta_wide_rows(oracle, parity_log, monkeypatch):
+    """The level-group sweep's dense-row mode (one row per CTA at a time, sums combined through
+    shared memory; chosen for >= 192 blocks per row, the Galerkin levels at 160^3), forced here on
+    every group-sweep operator of the 16^3 hierarchy: V-cycle 1e-12 and a whole first pass."""
+    monkeypatch.setenv("ED_GROUP_WIDE_ROW", "1")
+    cp = CubeProblem(n=16, nu=0.5)
+    P = _ref_problem(oracle, cp)
+    st = cp.seeded_state()
+    P.set_state(st.u, st.udot, st.p, st.pdot, st.v, st.vdot)
+    P.assemble_tangent()
+    planes = [P.tangent_plane(k) for k in range(4)]
+    ctx = api.Context(0)
+    ctx.set_block_system(*[_csr(m) for m in planes])
+    r = np.random.default_rng(12).uniform(-1, 1, cp.nv)
+    opts = cp.solver_options()
+    opts.amg_a = api.amg_options(3, 0)
+    zg, ig = ctx.amg_vcycle(r, 0, opts)
+    zr, ir = oracle.amg_vcycle_csr(planes[0], r, oracle.default_amg(3, 0))
+    assert ig["level_rows"] == ir["level_rows"], (ig, ir)
+    assert _rel(zg, zr) < 1e-12
+    ctx.close()
+    _first_pass_case(oracle, parity_log, "n16_nu0.5_first_pass_cta_wide_rows", cp, st)
