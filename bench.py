@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--nu", type=float, default=None)
     ap.add_argument("--dt", type=float, default=None)
     ap.add_argument("--cpu-sample-n", type=int, default=None, help="cube size of the CPU sample (default: the workload)")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (profiling runs)")
     ap.add_argument("--spmv-n", type=int, default=160,
                     help="cube size of the 160^3 leg (the metric's BSR SpMV GB/s, assembly, Newton pass); 0 skips it")
